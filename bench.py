@@ -1,0 +1,404 @@
+"""Benchmark: synthetic instances timed per second (both variants) on the
+full synthetic sweep (BASELINE.json configs[4]; the single-GPU line is the
+same sweep at N=1), plus the HBM roofline of the synthetic-kernel launches.
+
+A *step* is one batch of sweep instances per rank: for each instance the
+inputs are generated on the device (K0), the baseline (K1) and the
+local-memory variant (K2) are each run once and timed with CUDA events, and
+the two outputs are digested and compared bit for bit on the device.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): each step's global batch of N*B
+instances is split across ranks by estimated cost (no data-path
+collective); the per-instance labels (t_base, t_opt) are all-gathered over
+NCCL after the timed region, as SURVEY 8(e) prescribes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SWEEP_CAP = 1_000_000
+METRIC = "synthetic instances timed/sec (both variants)"
+UNIT = "instances/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=48, help="instances per rank per step")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- workload
+
+def workload(seed: int):
+    import paper_1412_6986_b200 as L
+
+    spec = L.SamplingSpec(max_instances=SWEEP_CAP, seed=seed)
+    table = L.select_instance_table(spec)
+    perm = np.random.default_rng(seed ^ 0x5EED).permutation(len(table))
+    return L, table, perm
+
+
+def step_rows(perm, step: int, world: int, batch: int):
+    g = perm[(step * world * batch) % len(perm):][: world * batch]
+    return g
+
+
+def shard_for_rank(L, table, rows, world: int, rank: int):
+    if world == 1:
+        return rows
+    cost = L.sweep.estimated_cost(table.records(rows))
+    return rows[L.sweep.shard_balanced(cost, world)[rank]]
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i", str(self.index),
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- CPU legs
+
+def cpu_sample(L, table, rows, budget_s: float):
+    """Oracle (plain-C restatement of interp.execute, all host threads) on a
+    bounded sample: for each sampled instance run both variants over a prefix
+    of its workgroups and extrapolate to the whole launch. Returns
+    (instances/s, cores, description)."""
+    import oracle
+
+    cores = os.cpu_count() or 1
+    spent, est_total, n_inst, wg_done = 0.0, 0.0, 0, 0
+    per_inst_budget = budget_s / 6
+    for r in rows:
+        inst = table.instance(int(r))
+        geo = L.emit_geometry(inst)
+        if geo.alloc_h * geo.alloc_w > 64 * 2**20:  # keep host input generation bounded
+            continue
+        p, lc = inst.params, inst.launch
+        nwg = (lc.grid_x // lc.wg_x) * (lc.grid_y // lc.wg_y)
+        a, b = oracle.make_inputs(inst)
+        feasible = L.footprint(inst).bytes <= 48 * 1024
+        take = max(1, min(nwg, cores))
+        elapsed = 0.0
+        while True:
+            t0 = time.perf_counter()
+            oracle.execute(inst, 0, a, b, nthreads=cores, wg_range=(0, take))
+            if feasible:
+                oracle.execute(inst, 1, a, b, nthreads=cores, wg_range=(0, take))
+            elapsed = time.perf_counter() - t0
+            if elapsed > per_inst_budget / 8 or take >= nwg:
+                break
+            take = min(nwg, take * 4)
+        spent += elapsed
+        est_total += elapsed * nwg / take
+        n_inst += 1
+        wg_done += take
+        if spent > budget_s or n_inst >= 6:
+            break
+    rate = n_inst / est_total if est_total > 0 else 0.0
+    desc = (f"oracle C port ({cores} threads): {n_inst} instances of the same sweep batch, both variants "
+            f"over a prefix of {wg_done} workgroups in total, time extrapolated linearly to all workgroups; "
+            f"{spent:.1f}s of CPU work")
+    return rate, cores, desc
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    L, table, perm = workload(args.seed)
+    rates = []
+    for s in range(args.warmup + args.steps):
+        rows = step_rows(perm, s, 1, args.batch)
+        rate, cores, desc = cpu_sample(L, table, rows, budget_s=max(2.0, args.cpu_seconds / max(1, args.steps)))
+        if s >= args.warmup:
+            rates.append(rate)
+    value = float(np.mean(rates)) if rates else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": (args.batch / value * 1e3) if value else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"full synthetic sweep SamplingSpec(max_instances={SWEEP_CAP}, seed={args.seed}), "
+                               f"batches of {args.batch} instances", "batch_per_rank": args.batch},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU leg
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    L, table, perm = workload(args.seed)
+    from paper_1412_6986_b200 import _lib
+
+    lib_stream = torch.cuda.ExternalStream(_lib.library_stream())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also JIT-free: all kernels are precompiled sm_100a SASS)
+    for s in range(args.warmup):
+        rows = shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+        L.measure_records(table.records(rows))
+
+    # ---- timed region: device-resident inputs (generated by K0 inside the step)
+    results = []
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(lib_stream)
+        for s in range(args.warmup, args.warmup + args.steps):
+            rows = shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+            res = L.measure_records(table.records(rows))
+            results.append((rows, res))
+        ev1.record(lib_stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
+    n_local = sum(len(r) for r, _ in results)
+    cnt = torch.tensor([n_local], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    max_ms = float(t.item())
+    n_total = int(cnt.item())
+    value = n_total / (max_ms / 1e3)
+
+    # ---- labels: NCCL all-gather of (row, t_base, t_opt) -- the only collective
+    rows_all = np.concatenate([r for r, _ in results])
+    res_all = np.concatenate([x for _, x in results])
+    lab = torch.tensor(np.stack([rows_all.astype(np.float64), res_all["t_base_ms"], res_all["t_opt_ms"]], 1),
+                       device="cuda", dtype=torch.float64)
+    if world > 1:
+        sizes = [torch.zeros(1, device="cuda", dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([lab.shape[0]], device="cuda", dtype=torch.int64))
+        mx = int(max(s.item() for s in sizes))
+        pad = torch.zeros((mx, 3), device="cuda", dtype=torch.float64)
+        pad[: lab.shape[0]] = lab
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad)
+        labels = torch.cat([b[: int(s.item())] for b, s in zip(bufs, sizes)])
+    else:
+        labels = lab
+    n_labels = int(labels.shape[0])
+
+    # ---- per-kernel accounting (the synthetic kernels are the dominant launches)
+    ok = res_all["t_base_ms"] > 0
+    ran_opt = res_all["t_opt_ms"] > 0
+    k_ms = float(res_all["t_base_ms"][ok].sum() + res_all["t_opt_ms"][ran_opt].sum())
+    k_bytes = float(res_all["alg_bytes"][ok].sum() + res_all["alg_bytes"][ran_opt].sum())
+    k_flops = float(res_all["alg_flops"][ok].sum() + res_all["alg_flops"][ran_opt].sum())
+    n_launch_kernels = int(ok.sum() + ran_opt.sum())
+    fill_ms = float(res_all["t_fill_ms"].sum())
+    verified = int(((res_all["mismatches"] == 0) & ran_opt).sum())
+    mismatched = int(((res_all["mismatches"] > 0) & ran_opt).sum())
+    failed = int((~ok).sum())
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+    gpu_launches = int(res_all["launches"].sum())
+
+    # ---- end to end: host (pinned) inputs -> H2D -> K1, K2, digest -> D2H outputs
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, L, table, perm, world, rank, barrier)
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu:
+        rows0 = step_rows(perm, args.warmup, world, args.batch)
+        rate, cores, desc = cpu_sample(L, table, rows0, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {
+            "workload": f"full synthetic sweep SamplingSpec(max_instances={SWEEP_CAP}, seed={args.seed}); "
+                        f"each step a seeded-random batch of {args.batch} instances per rank (both variants each)",
+            "batch_per_rank": args.batch, "out": "2048x2048", "parallelism": f"dp{world} (cost-balanced shards)",
+            "l2": "per-step working set >> 126 MB L2 (each instance writes 2x16 MB outputs plus its inputs)",
+        },
+        "instances_timed": n_total, "labels_gathered": n_labels, "verified_bitwise": verified,
+        "mismatched": mismatched, "failed": failed,
+        "kernel_ms": k_ms, "fill_ms": fill_ms, "step_ms_total": max_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "k_synth_base + k_synth_opt (all launches of the timed steps)",
+                     "note": "algorithmic bytes 4*(|U_in|+|U_in2|+out) per variant (SURVEY 8(d)) over summed "
+                             "CUDA-event kernel time; most sweep instances are fp32/LSU-issue bound"},
+        "fp32": {"achieved_tflops": k_flops / (k_ms / 1e3) / 1e12 if k_ms else 0.0},
+        "gpu_launches": gpu_launches,
+        "clocks": clocks.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, L, table, perm, world, rank, barrier):
+    """Same metric through the public host-buffer API: each instance's `in`
+    and `in2` come from pinned host memory and both outputs go back to pinned
+    host memory inside the timed region."""
+    import torch
+
+    steps = range(args.warmup, args.warmup + max(1, min(args.steps, 2)))
+    plan = []
+    host_in = {}
+    in2_host = None
+    pinned_bytes = 0
+    for s in steps:
+        rows = shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+        insts = table.instances(rows)
+        keep = []
+        for inst in insts:
+            g = L.emit_geometry(inst)
+            if g.alloc_h * g.alloc_w * 4 > 2**30 + 2**28:
+                continue
+            key = (g.alloc_h, g.alloc_w)
+            if key not in host_in:
+                dev = L.interp.device_fill(g.alloc_h, g.alloc_w, 0)[:, : g.alloc_w]
+                h = torch.empty((g.alloc_h, g.alloc_w), dtype=torch.float32, pin_memory=True)
+                h.copy_(dev)
+                host_in[key] = h
+                pinned_bytes += h.numel() * 4
+            keep.append((inst, host_in[key]))
+        plan.append(keep)
+    p0 = plan[0][0][0].params
+    in2_host = torch.empty((p0.in_h, p0.in_w), dtype=torch.float32, pin_memory=True)
+    in2_host.copy_(L.interp.device_fill(p0.in_h, p0.in_w, 1)[:, : p0.in_w])
+    out_b = torch.empty((p0.out_h, p0.out_w), dtype=torch.float32, pin_memory=True)
+    out_o = torch.empty_like(out_b)
+    torch.cuda.synchronize()
+    barrier()
+    h2d = d2h = n = 0
+    t0 = time.perf_counter()
+    for keep in plan:
+        insts = [i for i, _ in keep]
+        ins = [h for _, h in keep]
+        ms = L.measure_instances_host(insts, ins, [in2_host] * len(insts), out_base=[out_b] * len(insts),
+                                      out_opt=[out_o] * len(insts))
+        for m, h in zip(ms, ins):
+            h2d += h.numel() * 4 + in2_host.numel() * 4
+            d2h += out_b.numel() * 4 * (2 if m.t_opt_ms is not None else 1)
+        n += len(insts)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    import torch.distributed as dist
+
+    t = torch.tensor([el, float(n)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        el, n_all = float(mx.item()), float(t[1].item())
+    else:
+        n_all = float(n)
+    return {"value": n_all / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d / len(plan)),
+            "d2h_bytes_per_step": int(d2h / len(plan)), "steps": len(plan),
+            "note": "wall clock around synchronous C-ABI calls (lmt_measure_batch_host) with pinned host buffers"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

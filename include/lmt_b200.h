@@ -1,0 +1,171 @@
+/*
+ * lmt_b200.h -- C ABI of the B200-native lmtune hot path (liblmt_b200.so).
+ *
+ * The reference (lmtune, pure Python + numpy) has no FFI; its boundary is the
+ * public Python API (/root/reference/pkg/src/lmtune/__init__.py:9-84). Each
+ * entry point below replaces one reference function; the Python shim in
+ * paper_1412_6986_b200/ binds them with ctypes behind the reference's own
+ * signatures (INTEGRATION.md shows the binding a maintainer would add).
+ *
+ * Conventions
+ *  - plain pointers and sizes; no torch types. "d_" pointers are device
+ *    memory, "h_" pointers host memory. `stream` is a cudaStream_t (NULL =
+ *    the library's own stream for the calling device).
+ *  - every function returns LMT_OK (0) or an LMT_ERR_* code; the message of
+ *    the last failure on the calling thread is in lmt_last_error().
+ *    LMT_ERR_INVALID_INSTANCE maps to lmtune.errors.InvalidInstance
+ *    (errors.py:10-15), LMT_ERR_INFEASIBLE to OptimizationInfeasible
+ *    (errors.py:18-24), everything else to LmtuneError.
+ *  - device memory for inputs/outputs inside lmt_measure_batch* is owned by
+ *    the library (a per-device cache guarded by a mutex).
+ */
+#ifndef LMT_B200_H
+#define LMT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMT_OK 0
+#define LMT_ERR_INVALID_INSTANCE 1
+#define LMT_ERR_INFEASIBLE 2
+#define LMT_ERR_CUDA 3
+#define LMT_ERR_ARG 4
+#define LMT_ERR_TOO_LARGE 5
+
+/* TemplateParams + LaunchConfig (kernel_model.py:54-90), flattened.
+ * pattern: HomeAccessPattern declaration order (kernel_model.py:15-24):
+ *   0 xy_reuse 1 x_reuse_row 2 x_reuse_col 3 y_reuse_row 4 y_reuse_col
+ *   5 no_reuse_row_major 6 no_reuse_col_major
+ * stencil_shape: StencilShape order (kernel_model.py:27-30): 0 rect 1 diamond 2 star */
+typedef struct lmt_instance {
+    int32_t in_h, in_w, out_h, out_w;
+    int32_t pattern, n, m;
+    int32_t stencil_shape, stencil_radius;
+    int32_t num_comp_ilb, num_comp_ep;
+    int32_t num_coal_ilb, num_coal_ep;
+    int32_t num_uncoal_ilb, num_uncoal_ep;
+    int32_t grid_x, grid_y, wg_x, wg_y;
+} lmt_instance;
+
+/* DeviceDescriptor (device.py:11-37); the defaults are DEFAULT_DEVICE. */
+typedef struct lmt_device {
+    int32_t transaction_bytes, warp_size, element_bytes, lmem_capacity_bytes;
+    int32_t register_file_per_sm, max_regs_per_thread, max_warps_per_sm;
+    int32_t max_workgroups_per_sm, dram_latency_cycles, issue_cycles_per_op;
+} lmt_device;
+
+/* EmitGeometry (codegen.py:69-91) + Footprint (access_analysis.py:158-166)
+ * + the rest of AffineAccess (access_analysis.py:32-48). */
+typedef struct lmt_geometry {
+    int32_t pad, off_min_row, off_min_col;
+    int32_t r_rows, r_cols, r_cols_pad;
+    int32_t seg_elems, segs_per_row, num_segs, num_warps, lanes_per_warp;
+    int64_t alloc_h, alloc_w;
+    int32_t org_row_wu_x, org_row_wu_y, org_col_wu_x, org_col_wu_y;
+    int32_t row_i, row_j, col_i, col_j;
+    int64_t footprint_bytes;
+    int32_t num_offsets;
+} lmt_geometry;
+
+/* One measured instance (the GPU counterpart of cost_model.label_speedup,
+ * cost_model.py:144-158, which only *models* these times). */
+typedef struct lmt_measurement {
+    double t_base_ms;        /* CUDA-event time of the baseline kernel */
+    double t_opt_ms;         /* optimized kernel; < 0 when not run (infeasible) */
+    uint64_t digest_base;    /* order-independent digest of the baseline out */
+    uint64_t digest_opt;     /* same for the optimized out (0 if not run) */
+    int64_t mismatches;      /* elements whose bits differ base vs opt; -1 if not run */
+    double alg_bytes;        /* algorithmic bytes per variant */
+    double alg_flops;        /* algorithmic fp32 ops per variant (MAD = 2) */
+    double t_fill_ms;        /* input generation (K0) time; 0 when inputs were reused */
+    int32_t status;          /* LMT_OK, LMT_ERR_INFEASIBLE (opt skipped), or an error */
+    int32_t kernel_id;       /* which specialised kernel ran (diagnostics) */
+    int32_t launches;        /* kernels this instance launched (fill, K1, K2, digest) */
+    int32_t nstages;         /* shared-memory stages the optimized variant used */
+} lmt_measurement;
+
+typedef struct lmt_forest lmt_forest;
+
+/* flags for lmt_measure_batch */
+#define LMT_MEASURE_SKIP_OPT     0x1  /* run the baseline only */
+#define LMT_MEASURE_KEEP_OUTPUTS 0x2  /* leave the last instance's outs readable via lmt_last_outputs */
+#define LMT_MEASURE_ALLOW_LARGE_LMEM 0x4 /* run the optimized variant past the device lmem cap (B200 has 227 KB) */
+
+const char *lmt_version(void);
+const char *lmt_last_error(void);
+
+/* kernel_model.validate_instance (kernel_model.py:196-219). Returns the number
+ * of violations; their messages, joined by "; " as InvalidInstance does
+ * (errors.py:13-15), are written to msg (cap bytes, NUL-terminated). */
+int lmt_validate(const lmt_instance *inst, char *msg, int64_t cap);
+
+/* codegen.emit_geometry + access_analysis.footprint (codegen.py:94-132,
+ * access_analysis.py:184-213). */
+int lmt_emit_geometry(const lmt_instance *inst, const lmt_device *dev, lmt_geometry *out);
+
+/* interp._hash_fill / make_inputs (interp.py:22-38) into device memory:
+ * d_dst[r * pitch + c] = hash(r * cols + c + salt) for r < rows, c < cols. */
+int lmt_fill(float *d_dst, int64_t rows, int64_t cols, int64_t pitch, uint32_t salt, void *stream);
+
+/* interp.execute (interp.py:41-114) on the GPU. variant 0 = BASELINE
+ * (plain global loads), 1 = OPTIMIZED (region staged in shared memory by
+ * TMA). d_in is [in_rows, in_cols] with row pitch in_pitch floats (a multiple
+ * of 4, 16-byte aligned base); d_in2 is [in_h, in_w]; d_out [out_h, out_w].
+ * Asynchronous on `stream`. */
+int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant,
+                const float *d_in, int64_t in_rows, int64_t in_cols, int64_t in_pitch,
+                const float *d_in2, float *d_out, void *stream);
+
+/* The measurement path: for each instance generate its inputs on the device,
+ * run and time both variants with CUDA events, digest and compare the two
+ * outputs. Blocks until the batch is done. out[i] is always written; a failing
+ * instance gets a non-zero status (the batch continues, like build_dataset's
+ * skip log, dataset.py:264-281). Returns LMT_OK unless the arguments or the
+ * device are unusable. */
+int lmt_measure_batch(const lmt_instance *insts, int64_t n, const lmt_device *dev,
+                      int32_t flags, lmt_measurement *out);
+
+/* Same, end to end from host buffers: instance i's `in` is h_in[i]
+ * ([in_rows[i], in_cols[i]] contiguous, ideally pinned) and `in2` is h_in2[i];
+ * both are copied to the device inside the timed batch, and both outputs are
+ * copied back into h_out_base[i] / h_out_opt[i] (may be NULL to skip). */
+int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_device *dev,
+                           int32_t flags, const float *const *h_in, const int64_t *in_rows,
+                           const int64_t *in_cols, const float *const *h_in2,
+                           float *const *h_out_base, float *const *h_out_opt,
+                           lmt_measurement *out);
+
+/* Order-independent 64-bit digest of an fp32 device array (the digest in
+ * lmt_measurement). */
+int lmt_digest(const float *d, int64_t count, uint64_t *h_out, void *stream);
+
+/* Random-forest inference (forest.py:49-58, 208-219). Trees use the
+ * reference's node arrays (tree-local child indices, feature -1 = leaf);
+ * tree t owns nodes [tree_off[t], tree_off[t+1]). */
+int lmt_rf_create(const int32_t *feature, const double *threshold, const int32_t *left,
+                  const int32_t *right, const double *value, const int64_t *tree_off,
+                  int32_t ntrees, int32_t nfeat, lmt_forest **out);
+/* mean[r] = (sum over trees in tree order of leaf value) / T, bit-identical to
+ * forest.predict's acc / len(trees); votes[r] = number of trees whose leaf is
+ * > 0 (log2-speedup > 0), via warp ballot. d_votes may be NULL. */
+int lmt_rf_mean(const lmt_forest *f, const double *d_X, int64_t nrows, double *d_mean,
+                int32_t *d_votes, void *stream);
+/* Host-buffer convenience: copies X in, means (and votes) out. */
+int lmt_rf_mean_host(const lmt_forest *f, const double *h_X, int64_t nrows, double *h_mean,
+                     int32_t *h_votes);
+void lmt_rf_destroy(lmt_forest *f);
+
+/* Synchronise the library stream of the current device. */
+int lmt_sync(void);
+
+/* The library's stream on the current device (where lmt_measure_batch*
+ * launch), so callers can bracket a batch with their own CUDA events. */
+int lmt_get_stream(void **stream_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

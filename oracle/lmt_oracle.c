@@ -1,0 +1,417 @@
+/*
+ * lmt_oracle.c -- CPU ORACLE (test infrastructure only; see lmt_oracle.h).
+ *
+ * Plain-C restatement of the reference lmtune CPU path:
+ *   - index maps / geometry: kernel_model.py:115-219, access_analysis.py:51-62,
+ *     169-213, codegen.py:94-132
+ *   - input generation:      interp.py:22-38 (C twin: tests/_c_harness.py:57-60)
+ *   - both kernel variants:  interp.py:41-114 (semantics of codegen.py:240-333)
+ *   - random-forest mean:    forest.py:49-58, 208-218 (up to acc / T; the final
+ *                            2.0 ** mean is numpy's and stays in numpy)
+ *
+ * Compiled with -ffp-contract=off so that `acc * c1 + c2` is two roundings,
+ * exactly like numpy's float32 `acc * np.float32(c1) + np.float32(c2)`
+ * (interp.py:101).
+ */
+#include "lmt_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+static int is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+/* kernel_model.py:196-219 (validate_instance, incl. validate_params 173-193).
+ * Returns the number of violations. */
+int ora_validate(const ora_instance *p) {
+    int v = 0;
+    if (p->in_h < 1) v++;
+    if (p->in_w < 1) v++;
+    if (p->out_h < 1) v++;
+    if (p->out_w < 1) v++;
+    if (p->n < 1) v++;
+    if (p->m < 1) v++;
+    if (p->num_comp_ilb < 0) v++;
+    if (p->num_comp_ep < 0) v++;
+    if (p->num_coal_ilb < 0) v++;
+    if (p->num_coal_ep < 0) v++;
+    if (p->num_uncoal_ilb < 0) v++;
+    if (p->num_uncoal_ep < 0) v++;
+    if (p->stencil_radius < 0) v++;
+    if (!is_pow2(p->grid_x)) v++;
+    if (!is_pow2(p->grid_y)) v++;
+    if (!is_pow2(p->wg_x)) v++;
+    if (!is_pow2(p->wg_y)) v++;
+    if (p->wg_x > p->grid_x) v++;
+    if (p->wg_y > p->grid_y) v++;
+    if ((int64_t)p->wg_x * p->wg_y > 1024) v++;
+    if ((int64_t)p->grid_x * p->grid_y < 512) v++;
+    if (p->grid_x > 0 && p->out_w % p->grid_x != 0) v++;
+    if (p->grid_y > 0 && p->out_h % p->grid_y != 0) v++;
+    return v;
+}
+
+/* kernel_model.py:115-130: row-major (dr, dc) offsets of the stencil. */
+int ora_stencil_offsets(int shape, int r, int32_t *dr, int32_t *dc, int cap) {
+    int k = 0;
+    for (int a = -r; a <= r; a++) {
+        for (int b = -r; b <= r; b++) {
+            if (shape == 1 && abs(a) + abs(b) > r) continue;  /* diamond */
+            if (shape == 2 && a != 0 && b != 0) continue;    /* star */
+            if (k < cap) { dr[k] = a; dc[k] = b; }
+            k++;
+        }
+    }
+    return k;
+}
+
+/* access_analysis.py:51-62 (pattern_affine): row_wu_x, row_wu_y, row_i,
+ * row_j, col_wu_x, col_wu_y, col_i, col_j. */
+static int affine(int pattern, int n, int m, int32_t c[8]) {
+    static const int32_t tab[5][8] = {
+        {0, 0, 1, 0, 0, 0, 0, 1}, /* xy_reuse */
+        {0, 1, 0, 0, 0, 0, 0, 1}, /* x_reuse_row */
+        {0, 0, 0, 1, 0, 1, 0, 0}, /* x_reuse_col */
+        {1, 0, 0, 0, 0, 0, 0, 1}, /* y_reuse_row */
+        {0, 0, 0, 1, 1, 0, 0, 0}, /* y_reuse_col */
+    };
+    if (pattern >= 0 && pattern < 5) {
+        memcpy(c, tab[pattern], sizeof(tab[0]));
+        return 0;
+    }
+    if (pattern == 5) { /* no_reuse_row_major */
+        int32_t t[8] = {0, n, 1, 0, m, 0, 0, 1};
+        memcpy(c, t, sizeof(t));
+        return 0;
+    }
+    if (pattern == 6) { /* no_reuse_col_major */
+        int32_t t[8] = {0, m, 0, 1, n, 0, 1, 0};
+        memcpy(c, t, sizeof(t));
+        return 0;
+    }
+    return -1;
+}
+
+/* access_analysis.py:169-181 */
+static int64_t pad_col_span(int64_t col_span, int64_t tx_elems) {
+    if (col_span % tx_elems == 0) return col_span;
+    if (col_span > tx_elems) return (col_span / tx_elems + 1) * tx_elems;
+    int64_t b = 1;
+    while (b < col_span) b <<= 1; /* 1 << (col_span - 1).bit_length() */
+    return b;
+}
+
+/* access_analysis.py:184-213 (footprint) + codegen.py:94-132 (emit_geometry). */
+int ora_geometry_of(const ora_instance *p, const ora_device *dev, ora_geometry *g) {
+    int32_t c[8];
+    if (affine(p->pattern, p->n, p->m, c) != 0) return ORA_ERR_ARG;
+    if (p->stencil_radius < 0 || p->stencil_shape < 0 || p->stencil_shape > 2) return ORA_ERR_ARG;
+    int32_t dr[1024], dc[1024];
+    int K = ora_stencil_offsets(p->stencil_shape, p->stencil_radius, dr, dc, 1024);
+    if (K > 1024) return ORA_ERR_ARG;
+    int omin_r = dr[0], omax_r = dr[0], omin_c = dc[0], omax_c = dc[0];
+    for (int k = 1; k < K; k++) {
+        if (dr[k] < omin_r) omin_r = dr[k];
+        if (dr[k] > omax_r) omax_r = dr[k];
+        if (dc[k] < omin_c) omin_c = dc[k];
+        if (dc[k] > omax_c) omax_c = dc[k];
+    }
+    int64_t home_row_max = (int64_t)c[0] * (p->wg_x - 1) + (int64_t)c[1] * (p->wg_y - 1) +
+                           (int64_t)c[2] * (p->n - 1) + (int64_t)c[3] * (p->m - 1);
+    int64_t home_col_max = (int64_t)c[4] * (p->wg_x - 1) + (int64_t)c[5] * (p->wg_y - 1) +
+                           (int64_t)c[6] * (p->n - 1) + (int64_t)c[7] * (p->m - 1);
+    int64_t row_span = home_row_max + 1 + (omax_r - omin_r);
+    int64_t col_span = home_col_max + 1 + (omax_c - omin_c);
+    int64_t tx_elems = dev->transaction_bytes / dev->element_bytes;
+    int64_t padded = pad_col_span(col_span, tx_elems);
+    int64_t seg_elems = tx_elems < padded ? tx_elems : padded;
+    int64_t wg_size = (int64_t)p->wg_x * p->wg_y;
+    int64_t max_wu_x0 = (int64_t)p->out_w - p->wg_x;
+    int64_t max_wu_y0 = (int64_t)p->out_h - p->wg_y;
+    int64_t max_org_row = c[0] * max_wu_x0 + c[1] * max_wu_y0 + omin_r;
+    int64_t max_org_col = c[4] * max_wu_x0 + c[5] * max_wu_y0 + omin_c;
+    int pad = p->stencil_radius;
+    g->pad = pad;
+    g->off_min_row = omin_r;
+    g->off_min_col = omin_c;
+    g->r_rows = (int32_t)row_span;
+    g->r_cols = (int32_t)col_span;
+    g->r_cols_pad = (int32_t)padded;
+    g->seg_elems = (int32_t)seg_elems;
+    g->segs_per_row = (int32_t)(padded / seg_elems);
+    g->num_segs = (int32_t)(row_span * (padded / seg_elems));
+    g->num_warps = (int32_t)((wg_size + dev->warp_size - 1) / dev->warp_size);
+    g->lanes_per_warp = (int32_t)(dev->warp_size < wg_size ? dev->warp_size : wg_size);
+    g->alloc_h = pad + max_org_row + row_span;
+    g->alloc_w = pad + max_org_col + padded;
+    g->org_row_wu_x = c[0];
+    g->org_row_wu_y = c[1];
+    g->row_i = c[2];
+    g->row_j = c[3];
+    g->org_col_wu_x = c[4];
+    g->org_col_wu_y = c[5];
+    g->col_i = c[6];
+    g->col_j = c[7];
+    g->footprint_bytes = row_span * padded * dev->element_bytes;
+    g->num_offsets = K;
+    return ORA_OK;
+}
+
+/* interp.py:22-27 (_hash_fill); identical recurrence to _c_harness.py:57-60. */
+void ora_hash_fill(float *dst, int64_t count, uint32_t salt) {
+    for (int64_t i = 0; i < count; i++) {
+        uint32_t v = (uint32_t)((uint64_t)(i + (int64_t)salt) * 2654435761ull);
+        dst[i] = (float)((double)v / 4294967296.0 - 0.5);
+    }
+}
+
+/* codegen.py:58-66 (mad_constants) */
+static void mad_constants(int k, float *c1, float *c2) {
+    *c1 = (k % 2 == 0) ? 2.0f : 0.5f;
+    double a = (double)(1 + k % 5) / 64.0;
+    if (k % 2 == 1) a = -a;
+    *c2 = (float)a;
+}
+
+typedef struct exec_ctx {
+    const ora_instance *p;
+    const ora_geometry *g;
+    int variant;
+    const float *in;
+    int64_t in_rows, in_cols;
+    const float *in2;
+    float *out;
+    int32_t dr[1024], dc[1024];
+    int K;
+    int64_t wg_begin, wg_end;
+    int64_t next;           /* shared work counter (under lock) */
+    pthread_mutex_t lock;
+    int err;
+} exec_ctx;
+
+/* One workgroup, following interp.py:62-113 statement by statement. */
+static int run_workgroup(exec_ctx *x, int64_t gy, int64_t gx, float *region, float *acc) {
+    const ora_instance *p = x->p;
+    const ora_geometry *g = x->g;
+    const int64_t wg_w = p->wg_x, wg_h = p->wg_y, wg_size = wg_w * wg_h;
+    const int64_t nwx = p->out_w / p->grid_x, nwy = p->out_h / p->grid_y;
+    const int64_t in2_h = p->in_h, in2_w = p->in_w;
+    const int64_t pad = g->pad;
+    const int64_t rcp = g->r_cols_pad;
+    for (int64_t it_y = 0; it_y < nwy; it_y++) {
+        for (int64_t it_x = 0; it_x < nwx; it_x++) {
+            const int64_t wu_x0 = gx * (wg_w * nwx) + it_x * wg_w;
+            const int64_t wu_y0 = gy * (wg_h * nwy) + it_y * wg_h;
+            int64_t org_row = 0, org_col = 0;
+            if (x->variant == 1) {
+                /* interp.py:71-82: NaN-poisoned region, warp-cyclic segment copy */
+                org_row = g->org_row_wu_x * wu_x0 + g->org_row_wu_y * wu_y0 + g->off_min_row;
+                org_col = g->org_col_wu_x * wu_x0 + g->org_col_wu_y * wu_y0 + g->off_min_col;
+                const int64_t rsz = (int64_t)g->r_rows * rcp;
+                for (int64_t e = 0; e < rsz; e++) region[e] = NAN;
+                for (int64_t w = 0; w < g->num_warps; w++) {
+                    for (int64_t seg = w; seg < g->num_segs; seg += g->num_warps) {
+                        const int64_t seg_row = seg / g->segs_per_row;
+                        const int64_t seg_col = (seg % g->segs_per_row) * g->seg_elems;
+                        const int64_t r = org_row + seg_row + pad;
+                        for (int64_t e = 0; e < g->seg_elems; e++) {
+                            const int64_t c = org_col + seg_col + e + pad;
+                            if (r < 0 || r >= x->in_rows || c < 0 || c >= x->in_cols) return ORA_ERR_BOUNDS;
+                            region[seg_row * rcp + seg_col + e] = x->in[r * x->in_cols + c];
+                        }
+                    }
+                }
+            }
+            for (int64_t lane = 0; lane < wg_size; lane++) acc[lane] = 0.0f;
+            for (int64_t lane = 0; lane < wg_size; lane++) {
+                const int64_t wi_x = lane % wg_w, wi_y = lane / wg_w;
+                const int64_t glin = (gy * wg_h + wi_y) * p->grid_x + (gx * wg_w + wi_x);
+                const int64_t wu_x = wu_x0 + wi_x, wu_y = wu_y0 + wi_y;
+                float a = 0.0f;
+                for (int64_t i = 0; i < p->n; i++) {
+                    for (int64_t j = 0; j < p->m; j++) {
+                        const int64_t idx_o = g->org_row_wu_x * wu_x + g->org_row_wu_y * wu_y +
+                                              g->row_i * i + g->row_j * j;
+                        const int64_t idx_i = g->org_col_wu_x * wu_x + g->org_col_wu_y * wu_y +
+                                              g->col_i * i + g->col_j * j;
+                        for (int k = 0; k < x->K; k++) {
+                            if (x->variant == 0) {
+                                const int64_t r = idx_o + x->dr[k] + pad;
+                                const int64_t c = idx_i + x->dc[k] + pad;
+                                if (r < 0 || r >= x->in_rows || c < 0 || c >= x->in_cols) return ORA_ERR_BOUNDS;
+                                a = a + x->in[r * x->in_cols + c];
+                            } else {
+                                const int64_t rr = idx_o + x->dr[k] - org_row;
+                                const int64_t cc = idx_i + x->dc[k] - org_col;
+                                if (rr < 0 || rr >= g->r_rows) return ORA_ERR_BOUNDS;
+                                if (cc < 0 || cc >= rcp) return ORA_ERR_BOUNDS;
+                                a = a + region[rr * rcp + cc];
+                            }
+                        }
+                        for (int k = 0; k < p->num_comp_ilb; k++) {
+                            float c1, c2;
+                            mad_constants(k, &c1, &c2);
+                            a = a * c1 + c2;
+                        }
+                        for (int k = 0; k < p->num_coal_ilb; k++)
+                            a = a + x->in2[((i * p->m + j + k) % in2_h) * in2_w + glin % in2_w];
+                        for (int k = 0; k < p->num_uncoal_ilb; k++)
+                            a = a + x->in2[(glin % in2_h) * in2_w + (i * p->m + j + k) % in2_w];
+                    }
+                }
+                for (int k = 0; k < p->num_comp_ep; k++) {
+                    float c1, c2;
+                    mad_constants(p->num_comp_ilb + k, &c1, &c2);
+                    a = a * c1 + c2;
+                }
+                for (int k = 0; k < p->num_coal_ep; k++)
+                    a = a + x->in2[(((int64_t)p->n * p->m + k) % in2_h) * in2_w + glin % in2_w];
+                for (int k = 0; k < p->num_uncoal_ep; k++)
+                    a = a + x->in2[(glin % in2_h) * in2_w + ((int64_t)p->n * p->m + k) % in2_w];
+                x->out[wu_y * p->out_w + wu_x] = a;
+            }
+        }
+    }
+    return ORA_OK;
+}
+
+static void *exec_worker(void *arg) {
+    exec_ctx *x = (exec_ctx *)arg;
+    const ora_geometry *g = x->g;
+    const int64_t nwgx = x->p->grid_x / x->p->wg_x;
+    const int64_t wg_size = (int64_t)x->p->wg_x * x->p->wg_y;
+    float *region = NULL;
+    if (x->variant == 1) region = (float *)malloc(sizeof(float) * (size_t)g->r_rows * (size_t)g->r_cols_pad);
+    float *acc = (float *)malloc(sizeof(float) * (size_t)wg_size);
+    for (;;) {
+        int64_t w;
+        pthread_mutex_lock(&x->lock);
+        w = x->next++;
+        int stop = x->err != 0;
+        pthread_mutex_unlock(&x->lock);
+        if (stop || w >= x->wg_end) break;
+        int rc = run_workgroup(x, w / nwgx, w % nwgx, region, acc);
+        if (rc != ORA_OK) {
+            pthread_mutex_lock(&x->lock);
+            x->err = rc;
+            pthread_mutex_unlock(&x->lock);
+            break;
+        }
+    }
+    free(region);
+    free(acc);
+    return NULL;
+}
+
+/* interp.py:41-114 (execute). variant 0 = BASELINE, 1 = OPTIMIZED.
+ * `in` is [in_rows, in_cols] row-major (its own pitch, like the numpy array).
+ * Workgroups are linearised gy * (grid_x / wg_x) + gx; [wg_begin, wg_end)
+ * restricts the run to a contiguous range (wg_end < 0 means all). */
+int ora_execute(const ora_instance *p, const ora_device *dev, int variant,
+                const float *in, int64_t in_rows, int64_t in_cols,
+                const float *in2, float *out, int nthreads,
+                int64_t wg_begin, int64_t wg_end) {
+    ora_geometry g;
+    int rc = ora_geometry_of(p, dev, &g);
+    if (rc != ORA_OK) return rc;
+    if (p->wg_x <= 0 || p->wg_y <= 0 || p->grid_x % p->wg_x || p->grid_y % p->wg_y) return ORA_ERR_ARG;
+    if (p->out_w % p->grid_x || p->out_h % p->grid_y) return ORA_ERR_ARG;
+    exec_ctx *x = (exec_ctx *)calloc(1, sizeof(exec_ctx));
+    x->p = p;
+    x->g = &g;
+    x->variant = variant;
+    x->in = in;
+    x->in_rows = in_rows;
+    x->in_cols = in_cols;
+    x->in2 = in2;
+    x->out = out;
+    x->K = ora_stencil_offsets(p->stencil_shape, p->stencil_radius, x->dr, x->dc, 1024);
+    const int64_t nwg = (int64_t)(p->grid_x / p->wg_x) * (p->grid_y / p->wg_y);
+    x->wg_begin = wg_begin < 0 ? 0 : wg_begin;
+    x->wg_end = (wg_end < 0 || wg_end > nwg) ? nwg : wg_end;
+    x->next = x->wg_begin;
+    pthread_mutex_init(&x->lock, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t tids[256];
+    for (int t = 0; t < nthreads; t++) pthread_create(&tids[t], NULL, exec_worker, x);
+    for (int t = 0; t < nthreads; t++) pthread_join(tids[t], NULL);
+    rc = x->err;
+    pthread_mutex_destroy(&x->lock);
+    free(x);
+    return rc;
+}
+
+/* Order-independent 64-bit digest of an fp32 array: sum_i mix(i, bits_i).
+ * The product computes the same digest on the device (verification without
+ * a device->host copy of the whole output). */
+static uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint64_t ora_out_hash(const float *out, int64_t count) {
+    uint64_t h = 0;
+    for (int64_t i = 0; i < count; i++) {
+        uint32_t b;
+        memcpy(&b, &out[i], 4);
+        h += mix64((uint64_t)i * 0x9E3779B97F4A7C15ull + b);
+    }
+    return h;
+}
+
+typedef struct forest_ctx {
+    const int32_t *feature;
+    const double *threshold, *value;
+    const int32_t *left, *right;
+    const int64_t *tree_off;
+    int32_t ntrees, nfeat;
+    const double *X;
+    int64_t nrows;
+    double *mean;
+    int64_t chunk;
+    int tid, nthreads;
+} forest_ctx;
+
+static void *forest_worker(void *arg) {
+    forest_ctx *f = (forest_ctx *)arg;
+    for (int64_t r = f->tid; r < f->nrows; r += f->nthreads) {
+        const double *x = f->X + r * f->nfeat;
+        double acc = 0.0;
+        for (int32_t t = 0; t < f->ntrees; t++) {
+            const int64_t o = f->tree_off[t];
+            int64_t node = 0;
+            /* forest.py:49-58: walk while internal; x[f] <= thr goes left */
+            while (f->feature[o + node] >= 0) {
+                const int32_t ft = f->feature[o + node];
+                node = (x[ft] <= f->threshold[o + node]) ? f->left[o + node] : f->right[o + node];
+            }
+            acc = acc + f->value[o + node]; /* forest.py:216-217, tree order */
+        }
+        f->mean[r] = acc / (double)f->ntrees; /* forest.py:218 (inside 2.0 ** ...) */
+    }
+    return NULL;
+}
+
+/* forest.py:208-218 up to the mean. Tree t's nodes are [tree_off[t],
+ * tree_off[t+1]); left/right are tree-local node indices. */
+int ora_forest_mean(const int32_t *feature, const double *threshold,
+                    const int32_t *left, const int32_t *right, const double *value,
+                    const int64_t *tree_off, int32_t ntrees,
+                    const double *X, int64_t nrows, int32_t nfeat, double *mean_out,
+                    int nthreads) {
+    if (ntrees < 1 || nfeat < 1 || nrows < 0) return ORA_ERR_ARG;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t tids[256];
+    forest_ctx ctx[256];
+    for (int t = 0; t < nthreads; t++) {
+        ctx[t] = (forest_ctx){feature, threshold, value, left, right, tree_off, ntrees, nfeat,
+                              X, nrows, mean_out, 0, t, nthreads};
+        pthread_create(&tids[t], NULL, forest_worker, &ctx[t]);
+    }
+    for (int t = 0; t < nthreads; t++) pthread_join(tids[t], NULL);
+    return ORA_OK;
+}

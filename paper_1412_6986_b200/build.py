@@ -1,0 +1,59 @@
+"""Build liblmt_b200.so in-tree with nvcc for sm_100a.
+
+    python -m paper_1412_6986_b200.build
+
+Output: paper_1412_6986_b200/lib/liblmt_b200.so (git-ignored, travels to the
+GPU box with the repo snapshot). cudart is linked statically; the driver API
+entry point for TMA descriptors is resolved at run time
+(cudaGetDriverEntryPoint), so no libcuda is needed at build time.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc", "lmt_capi.cu")
+DEPS = [SRC, os.path.join(HERE, "csrc", "lmt_kernels.cuh"),
+        os.path.join(os.path.dirname(HERE), "include", "lmt_b200.h")]
+OUT = os.path.join(HERE, "lib", "liblmt_b200.so")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+    "-shared",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(OUT):
+        return False
+    t = os.path.getmtime(OUT)
+    return all(os.path.getmtime(d) <= t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
+    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", SRC]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(OUT + ".tmp", OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,895 @@
+// lmt_capi.cu -- host side of liblmt_b200.so: the C ABI declared in
+// include/lmt_b200.h. Validation, geometry, device-memory cache, TMA
+// descriptor encoding, kernel dispatch and CUDA-event timing.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lmt_b200.h"
+#include "lmt_kernels.cuh"
+
+#ifndef LMT_VERSION
+#define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
+#endif
+
+using namespace lmt;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return fail(LMT_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                        __LINE__);                                                           \
+    } while (0)
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+const lmt_device kDefaultDevice = {128, 32, 4, 48 * 1024, 32768, 63, 48, 8, 400, 4};
+
+// ------------------------------------------------------------ validation
+
+// kernel_model.py:173-219 (validate_params + validate_instance); same
+// messages in the same order, joined by "; " like InvalidInstance.
+std::vector<std::string> violations(const lmt_instance &p) {
+    std::vector<std::string> v;
+    char b[160];
+    const struct {
+        const char *n;
+        int32_t x;
+    } pos[] = {{"in_h", p.in_h}, {"in_w", p.in_w}, {"out_h", p.out_h},
+               {"out_w", p.out_w}, {"n", p.n},       {"m", p.m}};
+    for (auto &f : pos)
+        if (f.x < 1) { snprintf(b, sizeof b, "%s %d < 1", f.n, f.x); v.push_back(b); }
+    const struct {
+        const char *n;
+        int32_t x;
+    } cnt[] = {{"num_comp_ilb", p.num_comp_ilb},     {"num_comp_ep", p.num_comp_ep},
+               {"num_coal_ilb", p.num_coal_ilb},     {"num_coal_ep", p.num_coal_ep},
+               {"num_uncoal_ilb", p.num_uncoal_ilb}, {"num_uncoal_ep", p.num_uncoal_ep}};
+    for (auto &f : cnt)
+        if (f.x < 0) { snprintf(b, sizeof b, "%s %d < 0", f.n, f.x); v.push_back(b); }
+    if (p.stencil_radius < 0) {
+        snprintf(b, sizeof b, "stencil radius %d < 0", p.stencil_radius);
+        v.push_back(b);
+    }
+    const struct {
+        const char *n;
+        int32_t x;
+    } l[] = {{"grid_x", p.grid_x}, {"grid_y", p.grid_y}, {"wg_x", p.wg_x}, {"wg_y", p.wg_y}};
+    for (auto &f : l)
+        if (!is_pow2(f.x)) { snprintf(b, sizeof b, "%s %d is not a power of two", f.n, f.x); v.push_back(b); }
+    if (p.wg_x > p.grid_x) { snprintf(b, sizeof b, "wg_x %d > grid_x %d", p.wg_x, p.grid_x); v.push_back(b); }
+    if (p.wg_y > p.grid_y) { snprintf(b, sizeof b, "wg_y %d > grid_y %d", p.wg_y, p.grid_y); v.push_back(b); }
+    const int64_t wgs = (int64_t)p.wg_x * p.wg_y, gs = (int64_t)p.grid_x * p.grid_y;
+    if (wgs > 1024) { snprintf(b, sizeof b, "workgroup size %lld > 1024", (long long)wgs); v.push_back(b); }
+    if (gs < 512) { snprintf(b, sizeof b, "grid size %lld < 512", (long long)gs); v.push_back(b); }
+    if (p.grid_x > 0 && p.out_w % p.grid_x != 0) {
+        snprintf(b, sizeof b, "grid_x %d does not divide out_w %d", p.grid_x, p.out_w);
+        v.push_back(b);
+    }
+    if (p.grid_y > 0 && p.out_h % p.grid_y != 0) {
+        snprintf(b, sizeof b, "grid_y %d does not divide out_h %d", p.grid_y, p.out_h);
+        v.push_back(b);
+    }
+    return v;
+}
+
+// ------------------------------------------------------------- geometry
+
+// access_analysis.py:51-62
+bool pattern_affine(int pattern, int n, int m, int32_t c[8]) {
+    static const int32_t tab[5][8] = {{0, 0, 1, 0, 0, 0, 0, 1}, {0, 1, 0, 0, 0, 0, 0, 1},
+                                      {0, 0, 0, 1, 0, 1, 0, 0}, {1, 0, 0, 0, 0, 0, 0, 1},
+                                      {0, 0, 0, 1, 1, 0, 0, 0}};
+    if (pattern >= 0 && pattern < 5) { memcpy(c, tab[pattern], sizeof tab[0]); return true; }
+    if (pattern == 5) { const int32_t t[8] = {0, n, 1, 0, m, 0, 0, 1}; memcpy(c, t, sizeof t); return true; }
+    if (pattern == 6) { const int32_t t[8] = {0, m, 0, 1, n, 0, 1, 0}; memcpy(c, t, sizeof t); return true; }
+    return false;
+}
+
+// kernel_model.py:115-130
+int stencil_offsets(int shape, int r, std::vector<int> *dr, std::vector<int> *dc) {
+    int k = 0;
+    for (int a = -r; a <= r; a++)
+        for (int b = -r; b <= r; b++) {
+            if (shape == 1 && std::abs(a) + std::abs(b) > r) continue;
+            if (shape == 2 && a != 0 && b != 0) continue;
+            if (dr) { dr->push_back(a); dc->push_back(b); }
+            k++;
+        }
+    return k;
+}
+
+// access_analysis.py:169-181
+int64_t pad_col_span(int64_t span, int64_t tx) {
+    if (span % tx == 0) return span;
+    if (span > tx) return (span / tx + 1) * tx;
+    int64_t b = 1;
+    while (b < span) b <<= 1;
+    return b;
+}
+
+// access_analysis.py:184-213 + codegen.py:94-132
+int compute_geometry(const lmt_instance &p, const lmt_device &d, lmt_geometry *g) {
+    int32_t c[8];
+    if (!pattern_affine(p.pattern, p.n, p.m, c)) return fail(LMT_ERR_ARG, "unknown pattern %d", p.pattern);
+    if (p.stencil_shape < 0 || p.stencil_shape > 2) return fail(LMT_ERR_ARG, "unknown stencil shape %d", p.stencil_shape);
+    if (p.stencil_radius < 0 || p.stencil_radius > 64) return fail(LMT_ERR_ARG, "stencil radius %d out of range", p.stencil_radius);
+    if (d.transaction_bytes <= 0 || d.element_bytes <= 0 || d.warp_size <= 0) return fail(LMT_ERR_ARG, "bad device descriptor");
+    std::vector<int> dr, dc;
+    const int K = stencil_offsets(p.stencil_shape, p.stencil_radius, &dr, &dc);
+    const int omin_r = *std::min_element(dr.begin(), dr.end()), omax_r = *std::max_element(dr.begin(), dr.end());
+    const int omin_c = *std::min_element(dc.begin(), dc.end()), omax_c = *std::max_element(dc.begin(), dc.end());
+    const int64_t hrm = (int64_t)c[0] * (p.wg_x - 1) + (int64_t)c[1] * (p.wg_y - 1) + (int64_t)c[2] * (p.n - 1) +
+                        (int64_t)c[3] * (p.m - 1);
+    const int64_t hcm = (int64_t)c[4] * (p.wg_x - 1) + (int64_t)c[5] * (p.wg_y - 1) + (int64_t)c[6] * (p.n - 1) +
+                        (int64_t)c[7] * (p.m - 1);
+    const int64_t row_span = hrm + 1 + (omax_r - omin_r);
+    const int64_t col_span = hcm + 1 + (omax_c - omin_c);
+    const int64_t tx = d.transaction_bytes / d.element_bytes;
+    const int64_t padded = pad_col_span(col_span, tx);
+    const int64_t seg = std::min<int64_t>(tx, padded);
+    const int64_t wgs = (int64_t)p.wg_x * p.wg_y;
+    const int64_t mx0 = (int64_t)p.out_w - p.wg_x, my0 = (int64_t)p.out_h - p.wg_y;
+    const int64_t max_org_row = c[0] * mx0 + c[1] * my0 + omin_r;
+    const int64_t max_org_col = c[4] * mx0 + c[5] * my0 + omin_c;
+    g->pad = p.stencil_radius;
+    g->off_min_row = omin_r;
+    g->off_min_col = omin_c;
+    g->r_rows = (int32_t)row_span;
+    g->r_cols = (int32_t)col_span;
+    g->r_cols_pad = (int32_t)padded;
+    g->seg_elems = (int32_t)seg;
+    g->segs_per_row = (int32_t)(padded / seg);
+    g->num_segs = (int32_t)(row_span * (padded / seg));
+    g->num_warps = (int32_t)((wgs + d.warp_size - 1) / d.warp_size);
+    g->lanes_per_warp = (int32_t)std::min<int64_t>(d.warp_size, wgs);
+    g->alloc_h = p.stencil_radius + max_org_row + row_span;
+    g->alloc_w = p.stencil_radius + max_org_col + padded;
+    g->org_row_wu_x = c[0];
+    g->org_row_wu_y = c[1];
+    g->row_i = c[2];
+    g->row_j = c[3];
+    g->org_col_wu_x = c[4];
+    g->org_col_wu_y = c[5];
+    g->col_i = c[6];
+    g->col_j = c[7];
+    g->footprint_bytes = row_span * padded * d.element_bytes;
+    g->num_offsets = K;
+    return LMT_OK;
+}
+
+// ------------------------------------------------------ kernel dispatch
+
+using BaseFn = void (*)(const SynthArgs);
+using OptFn = void (*)(const CUtensorMap, const SynthArgs);
+
+struct KernelSet {
+    BaseFn base;
+    OptFn opt;
+    OptFn opt_wide;
+};
+
+// stencil ids: 0 point, 1 star1 (== diamond1), 2 star2, 3 diamond2, 4 rect1, 5 rect2, 6 generic
+const KernelSet kKernels[7] = {
+    {k_synth_base<0, 0>, k_synth_opt<0, 0, false>, k_synth_opt<0, 0, true>},
+    {k_synth_base<2, 1>, k_synth_opt<2, 1, false>, k_synth_opt<2, 1, true>},
+    {k_synth_base<2, 2>, k_synth_opt<2, 2, false>, k_synth_opt<2, 2, true>},
+    {k_synth_base<1, 2>, k_synth_opt<1, 2, false>, k_synth_opt<1, 2, true>},
+    {k_synth_base<0, 1>, k_synth_opt<0, 1, false>, k_synth_opt<0, 1, true>},
+    {k_synth_base<0, 2>, k_synth_opt<0, 2, false>, k_synth_opt<0, 2, true>},
+    {k_synth_base<-1, -1>, k_synth_opt<-1, -1, false>, k_synth_opt<-1, -1, true>},
+};
+
+int stencil_id(int shape, int r) {
+    if (r == 0) return 0;
+    if (r == 1) return shape == 0 ? 4 : 1;
+    if (r == 2) return shape == 0 ? 5 : (shape == 1 ? 3 : 2);
+    return 6;
+}
+
+// ------------------------------------------------------- device context
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+struct DevCtx {
+    int device = -1;
+    int sms = 0;
+    size_t smem_optin = 0;
+    cudaStream_t stream = nullptr;
+    float *in = nullptr;
+    size_t in_cap = 0;          // floats
+    int64_t in_rows = -1, in_cols = -1, in_pitch = -1;
+    float *in2 = nullptr;
+    size_t in2_cap = 0;
+    int64_t in2_h = -1, in2_w = -1;
+    float *outb = nullptr, *outo = nullptr;
+    size_t outb_cap = 0, outo_cap = 0;
+    unsigned long long *dres = nullptr;
+    size_t dres_cap = 0;        // instances
+    std::vector<cudaEvent_t> events;
+    bool attrs_set = false;
+};
+
+std::mutex g_mu;
+DevCtx g_ctx[64];
+
+int get_ctx(DevCtx **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(LMT_ERR_ARG, "device %d out of range", dev);
+    DevCtx &c = g_ctx[dev];
+    if (c.device < 0) {
+        CUDA_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+        int optin = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        c.smem_optin = (size_t)optin;
+        CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.device = dev;
+    }
+    if (!g_encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(LMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (!c.attrs_set) {
+        for (auto &k : kKernels) {
+            CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
+            CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt_wide),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
+        }
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_rf_mean),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        c.attrs_set = true;
+    }
+    *out = &c;
+    return LMT_OK;
+}
+
+template <class T>
+int ensure(T **p, size_t *cap, size_t need) {
+    if (*cap >= need && *p) return LMT_OK;
+    if (*p) CUDA_TRY(cudaFree(*p));
+    *p = nullptr;
+    *cap = 0;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(p), std::max<size_t>(need, 64) * sizeof(T)));
+    *cap = std::max<size_t>(need, 64);
+    return LMT_OK;
+}
+
+// ------------------------------------------------------ launch planning
+
+struct Plan {
+    lmt_geometry g;
+    SynthArgs A;
+    int sid;
+    bool feasible;      // footprint <= lmem cap (codegen.py:351)
+    bool wide;
+    size_t dyn_smem;
+    dim3 grid, block;
+    double alg_bytes, alg_flops;
+};
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// |U_in2|: union of the in2 cells the context reads touch.
+double in2_union(const lmt_instance &p) {
+    const int64_t H = p.in_h, W = p.in_w, nm = (int64_t)p.n * p.m;
+    const int64_t gs = (int64_t)p.grid_x * p.grid_y;
+    // glin takes every value in [0, grid_size), so glin % W covers
+    // [0, min(gs, W)) and glin % H covers [0, min(gs, H)).
+    const int64_t gcols = std::min(gs, W), grows = std::min(gs, H);
+    int64_t coal_rows = 0, coal_rows_lo = 0, uncoal_cols = 0, uncoal_cols_lo = 0;
+    auto count_set = [&](int64_t lo_count, int64_t extra_start, int64_t extra_count, int64_t mod, int64_t below,
+                         int64_t *in_range) {
+        std::vector<char> seen((size_t)mod, 0);
+        int64_t c = 0, c_lo = 0;
+        auto add = [&](int64_t r) {
+            if (!seen[(size_t)r]) { seen[(size_t)r] = 1; c++; if (r < below) c_lo++; }
+        };
+        for (int64_t t = 0; t < std::min(lo_count, mod); t++) add(t);
+        for (int64_t k = 0; k < std::min(extra_count, mod); k++) add((extra_start + k) % mod);
+        *in_range = c_lo;
+        return c;
+    };
+    if (p.num_coal_ilb > 0 || p.num_coal_ep > 0)
+        coal_rows = count_set(p.num_coal_ilb > 0 ? nm + p.num_coal_ilb - 1 : 0, nm, p.num_coal_ep, H, grows, &coal_rows_lo);
+    if (p.num_uncoal_ilb > 0 || p.num_uncoal_ep > 0)
+        uncoal_cols = count_set(p.num_uncoal_ilb > 0 ? nm + p.num_uncoal_ilb - 1 : 0, nm, p.num_uncoal_ep, W, gcols,
+                                &uncoal_cols_lo);
+    // coal cells: coal_rows x gcols; uncoal cells: grows x uncoal_cols;
+    // their intersection: (coal rows < grows) x (uncoal cols < gcols)
+    const double cells = (double)coal_rows * gcols + (double)grows * uncoal_cols - (double)coal_rows_lo * uncoal_cols_lo;
+    return cells;
+}
+
+// |U_in| in closed form: home rectangle dilated by the stencil.
+double in_union(const lmt_instance &p) {
+    const int64_t n = p.n, m = p.m, oh = p.out_h, ow = p.out_w, r = p.stencil_radius;
+    int64_t H = 0, W = 0;
+    switch (p.pattern) {
+        case 0: H = n; W = m; break;
+        case 1: H = oh; W = m; break;
+        case 2: H = m; W = oh; break;
+        case 3: H = ow; W = m; break;
+        case 4: H = m; W = ow; break;
+        case 5: H = oh * n; W = ow * m; break;
+        default: H = oh * m; W = ow * n; break;
+    }
+    if (r == 0) return (double)H * W;
+    if (p.stencil_shape == 0) return (double)(H + 2 * r) * (W + 2 * r);
+    if (p.stencil_shape == 2) return (double)H * W + 2.0 * r * (H + W);
+    return (double)H * W + 2.0 * r * (H + W) + 4.0 * (r * (r - 1) / 2);
+}
+
+int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan *pl, DevCtx *ctx) {
+    std::vector<std::string> v = violations(p);
+    if (!v.empty()) {
+        std::string m;
+        for (size_t i = 0; i < v.size(); i++) m += (i ? "; " : "") + v[i];
+        return fail(LMT_ERR_INVALID_INSTANCE, "%s", m.c_str());
+    }
+    int rc = compute_geometry(p, d, &pl->g);
+    if (rc) return rc;
+    const lmt_geometry &g = pl->g;
+    if (g.alloc_h * in_pitch >= (int64_t)1 << 31 || (int64_t)p.in_h * p.in_w >= (int64_t)1 << 31 ||
+        (int64_t)p.out_h * p.out_w >= (int64_t)1 << 31)
+        return fail(LMT_ERR_TOO_LARGE, "arrays exceed 2^31 elements");
+    std::vector<int> dr, dc;
+    const int K = stencil_offsets(p.stencil_shape, p.stencil_radius, &dr, &dc);
+    pl->sid = stencil_id(p.stencil_shape, p.stencil_radius);
+    if (pl->sid == 6 && K > kMaxGenericOffsets) return fail(LMT_ERR_TOO_LARGE, "stencil has %d > %d points", K, kMaxGenericOffsets);
+    SynthArgs &A = pl->A;
+    memset(&A, 0, sizeof A);
+    A.P = (int32_t)in_pitch;
+    A.H2 = p.in_h;
+    A.W2 = p.in_w;
+    A.out_w = p.out_w;
+    A.grid_x = p.grid_x;
+    A.N = p.n;
+    A.M = p.m;
+    A.nwx = p.out_w / p.grid_x;
+    A.nwy = p.out_h / p.grid_y;
+    A.comp_q = p.num_comp_ilb / 10;
+    A.comp_rem = p.num_comp_ilb % 10;
+    A.comp_ep = p.num_comp_ep;
+    A.comp_ep_phase = p.num_comp_ilb % 10;
+    A.coal_ilb = p.num_coal_ilb;
+    A.coal_ep = p.num_coal_ep;
+    A.uncoal_ilb = p.num_uncoal_ilb;
+    A.uncoal_ep = p.num_uncoal_ep;
+    const int64_t nm = (int64_t)p.n * p.m;
+    A.ep_row0 = (int32_t)(nm % p.in_h);
+    A.ep_col0 = (int32_t)(nm % p.in_w);
+    A.a[0] = g.org_row_wu_x; A.a[1] = g.org_row_wu_y; A.a[2] = g.row_i; A.a[3] = g.row_j;
+    A.a[4] = g.org_col_wu_x; A.a[5] = g.org_col_wu_y; A.a[6] = g.col_i; A.a[7] = g.col_j;
+    A.pad = g.pad;
+    A.off_min_row = g.off_min_row;
+    A.off_min_col = g.off_min_col;
+    A.K = K;
+    if (pl->sid == 6)
+        for (int k = 0; k < K; k++) { A.sdr[k] = (int8_t)dr[k]; A.sdc[k] = (int8_t)dc[k]; }
+    pl->block = dim3(p.wg_x, p.wg_y);
+    pl->grid = dim3(p.grid_x / p.wg_x, p.grid_y / p.wg_y);
+    pl->feasible = g.footprint_bytes <= d.lmem_capacity_bytes;
+
+    // TMA staging geometry: only the `col_span` columns are read
+    // (interp.py:94-97 bounds the reads by r_rows x r_cols_pad, and the
+    // footprint bounding box guarantees < col_span).
+    const int64_t rows = g.r_rows, cols = g.r_cols;
+    int64_t bw, ncc;
+    if (round_up(cols, 4) <= 256) {
+        bw = round_up(cols, 4);
+        if ((bw & 7) == 0 && bw + 4 <= 256) bw += 4;  // pitch = 4 * odd: column walks hit 8 banks, not 1
+        ncc = 1;
+        pl->wide = false;
+    } else {
+        bw = 256;
+        ncc = (cols + 255) / 256;
+        pl->wide = true;
+    }
+    const int64_t nrc = (rows + 255) / 256;
+    const int64_t bh = round_up((rows + nrc - 1) / nrc, 8);  // box stride stays 128-byte aligned
+    A.bw = (int32_t)bw;
+    A.bh = (int32_t)bh;
+    A.nrc = (int32_t)nrc;
+    A.ncc = (int32_t)ncc;
+    const int64_t stage_floats = ncc * nrc * bh * bw;
+    A.stage_floats = (int32_t)stage_floats;
+    A.stage_bytes = (uint32_t)(stage_floats * 4);
+    // stages: prefer overlap (>=2) and fill what the target occupancy leaves
+    const int64_t nit = (int64_t)A.nwx * A.nwy;
+    const int64_t warps = ((int64_t)p.wg_x * p.wg_y + 31) / 32;
+    const int64_t ctas = (int64_t)pl->grid.x * pl->grid.y;
+    const int64_t sms = ctx ? ctx->sms : 148;
+    int64_t want = std::min<int64_t>({32, std::max<int64_t>(1, 64 / warps), std::max<int64_t>(1, (ctas + sms - 1) / sms)});
+    const int64_t smem_cap = ctx ? (int64_t)ctx->smem_optin - 1024 : 227 * 1024;
+    const int64_t budget = (228 * 1024) / want - 1024;
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>(kMaxStages, budget / std::max<int64_t>(1, A.stage_bytes)));
+    if (S < 2 && 2 * (int64_t)A.stage_bytes <= smem_cap) S = 2;
+    S = std::max<int64_t>(1, std::min<int64_t>(S, nit));
+    while (S > 1 && S * (int64_t)A.stage_bytes > smem_cap) S--;
+    A.nstages = (int32_t)S;
+    pl->dyn_smem = (size_t)S * A.stage_bytes;
+    if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
+
+    pl->alg_bytes = 4.0 * (in_union(p) + in2_union(p) + (double)p.out_h * p.out_w);
+    const double per_wu = (double)nm * (K + 2.0 * p.num_comp_ilb + p.num_coal_ilb + p.num_uncoal_ilb) +
+                          2.0 * p.num_comp_ep + p.num_coal_ep + p.num_uncoal_ep;
+    pl->alg_flops = per_wu * p.out_h * p.out_w;
+    return LMT_OK;
+}
+
+int encode_tmap(CUtensorMap *map, const float *d_in, int64_t rows, int64_t cols, int64_t pitch, const Plan &pl) {
+    if (((uintptr_t)d_in & 15) || (pitch & 3)) return fail(LMT_ERR_ARG, "in must be 16-byte aligned with pitch %% 4 == 0");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+    cuuint32_t box[2] = {(cuuint32_t)pl.A.bw, (cuuint32_t)pl.A.bh};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(d_in), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LMT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) box %dx%d", (int)r, pl.A.bw, pl.A.bh);
+    return LMT_OK;
+}
+
+int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_rows, int64_t in_cols, int64_t pitch,
+                   const float *d_in2, float *d_out, cudaStream_t s) {
+    Plan pl = pl0;
+    pl.A.in = d_in;
+    pl.A.in2 = d_in2;
+    pl.A.out = d_out;
+    const KernelSet &ks = kKernels[pl.sid];
+    if (variant == 0) {
+        ks.base<<<pl.grid, pl.block, 0, s>>>(pl.A);
+    } else {
+        CUtensorMap map;
+        int rc = encode_tmap(&map, d_in, in_rows, in_cols, pitch, pl);
+        if (rc) return rc;
+        (pl.wide ? ks.opt_wide : ks.opt)<<<pl.grid, pl.block, pl.dyn_smem, s>>>(map, pl.A);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+int launch_fill(float *d, int64_t rows, int64_t cols, int64_t pitch, uint32_t salt, cudaStream_t s, int sms) {
+    const int64_t vecs = rows * (pitch / 4);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, (int64_t)sms * 16));
+    k_fill<<<(unsigned)blocks, 256, 0, s>>>(d, rows, cols, pitch, salt);
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+int launch_digest(const float *a, const float *b, int64_t count, unsigned long long *res, cudaStream_t s, int sms) {
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)sms * 8));
+    k_digest<<<(unsigned)blocks, 256, 0, s>>>(a, b, count, res);
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+lmt_device dev_or_default(const lmt_device *d) { return d ? *d : kDefaultDevice; }
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char *lmt_version(void) { return LMT_VERSION; }
+const char *lmt_last_error(void) { return g_err.c_str(); }
+
+int lmt_validate(const lmt_instance *inst, char *msg, int64_t cap) {
+    if (!inst) return -1;
+    std::vector<std::string> v = violations(*inst);
+    if (msg && cap > 0) {
+        std::string m;
+        for (size_t i = 0; i < v.size(); i++) m += (i ? "; " : "") + v[i];
+        snprintf(msg, (size_t)cap, "%s", m.c_str());
+    }
+    return (int)v.size();
+}
+
+int lmt_emit_geometry(const lmt_instance *inst, const lmt_device *dev, lmt_geometry *out) {
+    if (!inst || !out) return fail(LMT_ERR_ARG, "null argument");
+    return compute_geometry(*inst, dev_or_default(dev), out);
+}
+
+int lmt_fill(float *d_dst, int64_t rows, int64_t cols, int64_t pitch, uint32_t salt, void *stream) {
+    if (!d_dst || rows < 0 || cols < 0 || pitch < cols || (pitch & 3)) return fail(LMT_ERR_ARG, "bad fill arguments");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    return launch_fill(d_dst, rows, cols, pitch, salt, stream ? (cudaStream_t)stream : c->stream, c->sms);
+}
+
+int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, const float *d_in, int64_t in_rows,
+                int64_t in_cols, int64_t in_pitch, const float *d_in2, float *d_out, void *stream) {
+    if (!inst || !d_in || !d_in2 || !d_out) return fail(LMT_ERR_ARG, "null argument");
+    if (variant != 0 && variant != 1) return fail(LMT_ERR_ARG, "variant must be 0 or 1");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    const lmt_device d = dev_or_default(dev);
+    Plan pl;
+    rc = make_plan(*inst, d, in_pitch, &pl, c);
+    if (rc) return rc;
+    if (in_rows < pl.g.alloc_h || in_cols < pl.g.alloc_w)
+        return fail(LMT_ERR_ARG, "in is %lldx%lld, instance needs %lldx%lld", (long long)in_rows, (long long)in_cols,
+                    (long long)pl.g.alloc_h, (long long)pl.g.alloc_w);
+    // interp.execute runs the optimized variant whatever its footprint; the
+    // only hard limit here is that one staged region fits the SM's shared memory.
+    if (variant == 1 && (int64_t)pl.A.stage_bytes > (int64_t)c->smem_optin - 1024)
+        return fail(LMT_ERR_INFEASIBLE, "local-memory footprint %lld bytes exceeds capacity %d",
+                    (long long)pl.g.footprint_bytes, (int)c->smem_optin - 1024);
+    return launch_variant(pl, variant, d_in, in_rows, in_cols, in_pitch, d_in2, d_out,
+                          stream ? (cudaStream_t)stream : c->stream);
+}
+
+int lmt_digest(const float *d, int64_t count, uint64_t *h_out, void *stream) {
+    if (!d || !h_out || count < 0) return fail(LMT_ERR_ARG, "bad digest arguments");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    rc = ensure(&c->dres, &c->dres_cap, 3);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->dres, 0, 3 * sizeof(unsigned long long), s));
+    rc = launch_digest(d, nullptr, count, c->dres, s, c->sms);
+    if (rc) return rc;
+    unsigned long long h[3];
+    CUDA_TRY(cudaMemcpyAsync(h, c->dres, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *h_out = h[0];
+    return LMT_OK;
+}
+
+static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
+                        const float *const *h_in, const int64_t *h_rows, const int64_t *h_cols,
+                        const float *const *h_in2, float *const *h_ob, float *const *h_oo, lmt_measurement *out) {
+    if (!insts || !out || n < 0) return fail(LMT_ERR_ARG, "bad measure arguments");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    const lmt_device d = dev_or_default(dev);
+    cudaStream_t s = c->stream;
+    const bool host = h_in != nullptr;
+    rc = ensure(&c->dres, &c->dres_cap, (size_t)std::max<int64_t>(n, 1) * 3);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->dres, 0, (size_t)std::max<int64_t>(n, 1) * 3 * sizeof(unsigned long long), s));
+    const size_t nev = (size_t)n * 4;
+    while (c->events.size() < nev) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        c->events.push_back(e);
+    }
+    std::vector<char> ran_base((size_t)n, 0), ran_opt((size_t)n, 0), filled((size_t)n, 0);
+    for (int64_t i = 0; i < n; i++) {
+        lmt_measurement &m = out[i];
+        memset(&m, 0, sizeof m);
+        m.t_opt_ms = -1.0;
+        m.mismatches = -1;
+        const lmt_instance &p = insts[i];
+        // physical pitch: the logical pitch rounded to 16 bytes (TMA stride rule)
+        lmt_geometry g0;
+        int grc = LMT_OK;
+        {
+            std::vector<std::string> v = violations(p);
+            if (!v.empty()) {
+                std::string msg;
+                for (size_t k = 0; k < v.size(); k++) msg += (k ? "; " : "") + v[k];
+                m.status = fail(LMT_ERR_INVALID_INSTANCE, "%s", msg.c_str());
+                continue;
+            }
+            grc = compute_geometry(p, d, &g0);
+            if (grc) { m.status = grc; continue; }
+        }
+        const int64_t rows = host ? h_rows[i] : g0.alloc_h;
+        const int64_t cols = host ? h_cols[i] : g0.alloc_w;
+        const int64_t pitch = round_up(cols, 4);
+        Plan pl;
+        rc = make_plan(p, d, pitch, &pl, c);
+        if (rc) { m.status = rc; continue; }
+        if (rows < pl.g.alloc_h || cols < pl.g.alloc_w) {
+            m.status = fail(LMT_ERR_ARG, "instance %lld: in too small", (long long)i);
+            continue;
+        }
+        m.alg_bytes = pl.alg_bytes;
+        m.alg_flops = pl.alg_flops;
+        m.kernel_id = pl.sid * 2 + (pl.wide ? 1 : 0);
+        cudaEvent_t *ev = &c->events[(size_t)i * 4];
+        // ---- inputs (make_inputs, interp.py:30-38)
+        const size_t need_in = (size_t)(rows * pitch), need_out = (size_t)p.out_h * p.out_w;
+        const size_t need_in2 = (size_t)p.in_h * p.in_w;
+        if (host || c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in) {
+            if (need_in > c->in_cap) {
+                CUDA_TRY(cudaStreamSynchronize(s));
+                size_t fr = 0, tot = 0;
+                CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+                if (need_in * 4 + ((size_t)256 << 20) > fr + c->in_cap * 4) {
+                    m.status = fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i, need_in * 4);
+                    continue;
+                }
+                rc = ensure(&c->in, &c->in_cap, need_in);
+                if (rc) return rc;
+            }
+            CUDA_TRY(cudaEventRecord(ev[3], s));
+            if (host) {
+                CUDA_TRY(cudaMemcpy2DAsync(c->in, (size_t)pitch * 4, h_in[i], (size_t)cols * 4, (size_t)cols * 4,
+                                           (size_t)rows, cudaMemcpyHostToDevice, s));
+            } else {
+                rc = launch_fill(c->in, rows, cols, pitch, 0, s, c->sms);
+                if (rc) return rc;
+            }
+            m.launches += host ? 0 : 1;
+            c->in_rows = host ? -1 : rows;
+            c->in_cols = host ? -1 : cols;
+            c->in_pitch = host ? -1 : pitch;
+            filled[(size_t)i] = 1;
+        }
+        if (host || c->in2_h != p.in_h || c->in2_w != p.in_w || !c->in2) {
+            rc = ensure(&c->in2, &c->in2_cap, need_in2);
+            if (rc) return rc;
+            if (!filled[(size_t)i]) { CUDA_TRY(cudaEventRecord(ev[3], s)); filled[(size_t)i] = 1; }
+            if (host) {
+                CUDA_TRY(cudaMemcpyAsync(c->in2, h_in2[i], need_in2 * 4, cudaMemcpyHostToDevice, s));
+            } else {
+                rc = launch_fill(c->in2, p.in_h, p.in_w, p.in_w, 1, s, c->sms);
+                if (rc) return rc;
+                m.launches += 1;
+            }
+            c->in2_h = host ? -1 : p.in_h;
+            c->in2_w = host ? -1 : p.in_w;
+        }
+        rc = ensure(&c->outb, &c->outb_cap, need_out);
+        if (rc) return rc;
+        rc = ensure(&c->outo, &c->outo_cap, need_out);
+        if (rc) return rc;
+        // ---- K1, K2 timed with events on the launching stream
+        CUDA_TRY(cudaEventRecord(ev[0], s));
+        rc = launch_variant(pl, 0, c->in, rows, cols, pitch, c->in2, c->outb, s);
+        if (rc) { m.status = rc; continue; }
+        CUDA_TRY(cudaEventRecord(ev[1], s));
+        ran_base[(size_t)i] = 1;
+        m.launches += 1;
+        m.nstages = pl.A.nstages;
+        const bool run_opt = !(flags & LMT_MEASURE_SKIP_OPT) &&
+                             (pl.feasible || ((flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
+                                              (int64_t)pl.A.stage_bytes <= (int64_t)c->smem_optin - 1024));
+        if (run_opt) {
+            rc = launch_variant(pl, 1, c->in, rows, cols, pitch, c->in2, c->outo, s);
+            if (rc) { m.status = rc; continue; }
+            CUDA_TRY(cudaEventRecord(ev[2], s));
+            ran_opt[(size_t)i] = 1;
+            m.launches += 1;
+        } else if (!pl.feasible) {
+            m.status = LMT_ERR_INFEASIBLE;
+        }
+        rc = launch_digest(c->outb, run_opt ? c->outo : nullptr, (int64_t)need_out, c->dres + i * 3, s, c->sms);
+        if (rc) return rc;
+        m.launches += 1;
+        if (host && h_ob && h_ob[i])
+            CUDA_TRY(cudaMemcpyAsync(h_ob[i], c->outb, need_out * 4, cudaMemcpyDeviceToHost, s));
+        if (host && run_opt && h_oo && h_oo[i])
+            CUDA_TRY(cudaMemcpyAsync(h_oo[i], c->outo, need_out * 4, cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<unsigned long long> res((size_t)std::max<int64_t>(n, 1) * 3);
+    CUDA_TRY(cudaMemcpyAsync(res.data(), c->dres, res.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n; i++) {
+        lmt_measurement &m = out[i];
+        cudaEvent_t *ev = &c->events[(size_t)i * 4];
+        float ms = 0.0f;
+        if (ran_base[(size_t)i]) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+            m.t_base_ms = ms;
+            m.digest_base = res[(size_t)i * 3];
+            if (filled[(size_t)i]) {
+                CUDA_TRY(cudaEventElapsedTime(&ms, ev[3], ev[0]));
+                m.t_fill_ms = ms;
+            }
+        }
+        if (ran_opt[(size_t)i]) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+            m.t_opt_ms = ms;
+            m.digest_opt = res[(size_t)i * 3 + 1];
+            m.mismatches = (int64_t)res[(size_t)i * 3 + 2];
+        }
+    }
+    return LMT_OK;
+}
+
+int lmt_measure_batch(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
+                      lmt_measurement *out) {
+    return measure_impl(insts, n, dev, flags, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
+}
+
+int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
+                           const float *const *h_in, const int64_t *in_rows, const int64_t *in_cols,
+                           const float *const *h_in2, float *const *h_out_base, float *const *h_out_opt,
+                           lmt_measurement *out) {
+    if (!h_in || !in_rows || !in_cols || !h_in2) return fail(LMT_ERR_ARG, "host inputs required");
+    return measure_impl(insts, n, dev, flags, h_in, in_rows, in_cols, h_in2, h_out_base, h_out_opt, out);
+}
+
+int lmt_get_stream(void **stream_out) {
+    if (!stream_out) return fail(LMT_ERR_ARG, "null argument");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    *stream_out = (void *)c->stream;
+    return LMT_OK;
+}
+
+int lmt_sync(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LMT_OK;
+}
+
+// ------------------------------------------------------------ forest
+
+struct lmt_forest {
+    int device = -1;
+    int32_t ntrees = 0, nfeat = 0;
+    RfNode *nodes = nullptr;
+    int64_t *tree_off = nullptr;
+    int32_t *cached_off = nullptr;
+    int32_t ncached = 0;
+};
+
+int lmt_rf_create(const int32_t *feature, const double *threshold, const int32_t *left, const int32_t *right,
+                  const double *value, const int64_t *tree_off, int32_t ntrees, int32_t nfeat, lmt_forest **out) {
+    if (!feature || !threshold || !left || !right || !value || !tree_off || !out || ntrees < 1 || nfeat < 1)
+        return fail(LMT_ERR_ARG, "bad forest arguments");
+    // breadth-first renumbering per tree: the two children of a node become
+    // adjacent (right = left + 1) and the top levels form a prefix
+    std::vector<RfNode> flat;
+    std::vector<int64_t> off((size_t)ntrees + 1, 0);
+    std::vector<int32_t> coff((size_t)ntrees + 1, 0);
+    for (int32_t t = 0; t < ntrees; t++) {
+        const int64_t b = tree_off[t], e = tree_off[t + 1];
+        const int64_t nn = e - b;
+        if (nn < 1) return fail(LMT_ERR_ARG, "tree %d is empty", t);
+        std::vector<int64_t> newid((size_t)nn, -1), order;
+        order.reserve((size_t)nn);
+        newid[0] = 0;
+        order.push_back(0);
+        int64_t next = 1;
+        for (size_t q = 0; q < order.size(); q++) {
+            const int64_t u = order[q];
+            if (feature[b + u] < 0) continue;
+            if (feature[b + u] >= nfeat) return fail(LMT_ERR_ARG, "tree %d node %lld: feature out of range", t, (long long)u);
+            const int64_t l = left[b + u], r = right[b + u];
+            if (l < 0 || l >= nn || r < 0 || r >= nn || newid[l] >= 0 || newid[r] >= 0 || l == r)
+                return fail(LMT_ERR_ARG, "tree %d node %lld: bad children", t, (long long)u);
+            newid[l] = next++;
+            newid[r] = next++;
+            order.push_back(l);
+            order.push_back(r);
+        }
+        off[(size_t)t] = (int64_t)flat.size();
+        std::vector<RfNode> tn(order.size());
+        for (size_t q = 0; q < order.size(); q++) {
+            const int64_t u = order[q];
+            RfNode nd;
+            if (feature[b + u] < 0) {
+                nd.v = value[b + u];
+                nd.feature = -1;
+                nd.left = -1;
+            } else {
+                nd.v = threshold[b + u];
+                nd.feature = feature[b + u];
+                nd.left = (int32_t)newid[left[b + u]];
+            }
+            tn[(size_t)newid[u]] = nd;
+        }
+        flat.insert(flat.end(), tn.begin(), tn.end());
+    }
+    off[(size_t)ntrees] = (int64_t)flat.size();
+    // shared-memory prefix per tree (top levels), kRfSmemNodes in total
+    const int32_t per = kRfSmemNodes / ntrees;
+    for (int32_t t = 0; t < ntrees; t++)
+        coff[(size_t)t + 1] = coff[(size_t)t] + (int32_t)std::min<int64_t>(per, off[(size_t)t + 1] - off[(size_t)t]);
+    lmt_forest *f = new lmt_forest();
+    CUDA_TRY(cudaGetDevice(&f->device));
+    f->ntrees = ntrees;
+    f->nfeat = nfeat;
+    f->ncached = coff[(size_t)ntrees];
+    cudaError_t e1 = cudaMalloc(&f->nodes, flat.size() * sizeof(RfNode));
+    cudaError_t e2 = cudaMalloc(&f->tree_off, off.size() * sizeof(int64_t));
+    cudaError_t e3 = cudaMalloc(&f->cached_off, coff.size() * sizeof(int32_t));
+    if (e1 || e2 || e3) { lmt_rf_destroy(f); return fail(LMT_ERR_CUDA, "forest allocation failed"); }
+    CUDA_TRY(cudaMemcpy(f->nodes, flat.data(), flat.size() * sizeof(RfNode), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(f->tree_off, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(f->cached_off, coff.data(), coff.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    *out = f;
+    return LMT_OK;
+}
+
+int lmt_rf_mean(const lmt_forest *f, const double *d_X, int64_t nrows, double *d_mean, int32_t *d_votes, void *stream) {
+    if (!f || (!d_X && nrows > 0) || (!d_mean && nrows > 0) || nrows < 0) return fail(LMT_ERR_ARG, "bad rf arguments");
+    if (nrows == 0) return LMT_OK;
+    DevCtx *c;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int rc = get_ctx(&c);
+        if (rc) return rc;
+    }
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    const int64_t warps = (nrows + 0);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)c->sms * 8));
+    const size_t smem = (size_t)f->ncached * sizeof(RfNode);
+    k_rf_mean<<<(unsigned)blocks, 256, smem, s>>>(f->nodes, f->tree_off, f->cached_off, f->ntrees, d_X, nrows, f->nfeat,
+                                                  d_mean, d_votes);
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+int lmt_rf_mean_host(const lmt_forest *f, const double *h_X, int64_t nrows, double *h_mean, int32_t *h_votes) {
+    if (!f || nrows < 0) return fail(LMT_ERR_ARG, "bad rf arguments");
+    if (nrows == 0) return LMT_OK;
+    DevCtx *c;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int rc = get_ctx(&c);
+        if (rc) return rc;
+    }
+    double *dX = nullptr, *dm = nullptr;
+    int32_t *dv = nullptr;
+    CUDA_TRY(cudaMallocAsync(&dX, (size_t)nrows * f->nfeat * sizeof(double), c->stream));
+    CUDA_TRY(cudaMallocAsync(&dm, (size_t)nrows * sizeof(double), c->stream));
+    if (h_votes) CUDA_TRY(cudaMallocAsync(&dv, (size_t)nrows * sizeof(int32_t), c->stream));
+    CUDA_TRY(cudaMemcpyAsync(dX, h_X, (size_t)nrows * f->nfeat * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    int rc = lmt_rf_mean(f, dX, nrows, dm, dv, c->stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(h_mean, dm, (size_t)nrows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (h_votes) CUDA_TRY(cudaMemcpyAsync(h_votes, dv, (size_t)nrows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaFreeAsync(dX, c->stream));
+    CUDA_TRY(cudaFreeAsync(dm, c->stream));
+    if (dv) CUDA_TRY(cudaFreeAsync(dv, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LMT_OK;
+}
+
+void lmt_rf_destroy(lmt_forest *f) {
+    if (!f) return;
+    if (f->nodes) cudaFree(f->nodes);
+    if (f->tree_off) cudaFree(f->tree_off);
+    if (f->cached_off) cudaFree(f->cached_off);
+    delete f;
+}
+
+}  // extern "C"

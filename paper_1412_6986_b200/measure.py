@@ -1,0 +1,171 @@
+"""Measured labels: run and time both variants of many instances on the GPU.
+
+This is the B200 counterpart of the reference's *modelled* label
+(cost_model.kernel_time / label_speedup, cost_model.py:94-158): instead of
+estimating T_baseline / T_optimized it executes both kernels, times each with
+CUDA events, and verifies that the two outputs are bitwise identical (the
+reference's own invariant, test_interp.py:70-110) through on-device digests.
+
+Failures are per instance, as in build_dataset's skip log
+(dataset.py:264-281): a failing instance gets ``status != 0`` and an error
+string; the batch carries on.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import (
+    LMT_ERR_INFEASIBLE,
+    LMT_OK,
+    MEASURE_ALLOW_LARGE_LMEM,
+    MEASURE_SKIP_OPT,
+    CMeasurement,
+    check,
+    last_error,
+    lib,
+)
+from .device import DEFAULT_DEVICE
+from .geometry import c_device
+from .kernel_model import to_c_array
+
+STATUS_NAMES = {0: "ok", 1: "InvalidInstance", 2: "OptimizationInfeasible", 3: "CudaError",
+                4: "BadArgument", 5: "TooLarge"}
+
+
+@dataclass(frozen=True)
+class Measurement:
+    instance: object
+    t_base_ms: float
+    t_opt_ms: float | None          # None: optimized variant infeasible / not run
+    digest_base: int
+    digest_opt: int | None
+    mismatches: int                 # -1 when the optimized variant did not run
+    alg_bytes: float                # algorithmic bytes per variant
+    alg_flops: float                # algorithmic fp32 ops per variant
+    t_fill_ms: float
+    status: int
+    kernel_id: int
+    launches: int
+    nstages: int
+
+    @property
+    def ok(self) -> bool:
+        return self.status in (LMT_OK, LMT_ERR_INFEASIBLE) and self.t_base_ms > 0
+
+    @property
+    def verified(self) -> bool:
+        """Both variants ran and agree bit for bit."""
+        return self.t_opt_ms is not None and self.mismatches == 0
+
+    @property
+    def speedup(self) -> float:
+        """Measured T_baseline / T_optimized; 0.0 when the optimized variant is
+        infeasible, matching label_speedup's convention (cost_model.py:154-157)."""
+        if self.t_opt_ms is None or self.t_opt_ms <= 0:
+            return 0.0
+        return self.t_base_ms / self.t_opt_ms
+
+    @property
+    def beneficial(self) -> bool:
+        return self.speedup > 1.0
+
+
+def _convert(instances, raw) -> list[Measurement]:
+    out = []
+    for inst, m in zip(instances, raw):
+        ran_opt = m.t_opt_ms >= 0
+        out.append(Measurement(
+            instance=inst, t_base_ms=m.t_base_ms, t_opt_ms=m.t_opt_ms if ran_opt else None,
+            digest_base=int(m.digest_base), digest_opt=int(m.digest_opt) if ran_opt else None,
+            mismatches=int(m.mismatches), alg_bytes=m.alg_bytes, alg_flops=m.alg_flops,
+            t_fill_ms=m.t_fill_ms, status=int(m.status), kernel_id=int(m.kernel_id),
+            launches=int(m.launches), nstages=int(m.nstages),
+        ))
+    return out
+
+
+def measure_raw(instances, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False,
+                chunk: int = 4096):
+    """lmt_measure_batch over ``instances``; returns the raw ctypes records."""
+    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    cdev = c_device(dev)
+    res = []
+    for s in range(0, len(instances), chunk):
+        part = instances[s: s + chunk]
+        arr = to_c_array(part)
+        out = (CMeasurement * max(len(part), 1))()
+        check(lib().lmt_measure_batch(arr, len(part), ctypes.byref(cdev), flags, out), what="measure_batch")
+        res.extend(out[: len(part)])
+    return res
+
+
+def measure_records(records, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False):
+    """Measure an int32 [n, 19] record table (sweep.InstanceTable.records);
+    returns a numpy structured view of the lmt_measurement records."""
+    from .sweep import records_to_c
+
+    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    n = len(records)
+    arr = records_to_c(records)
+    out = (CMeasurement * max(n, 1))()
+    check(lib().lmt_measure_batch(arr, n, ctypes.byref(c_device(dev)), flags, out), what="measure_batch")
+    return np.frombuffer(out, dtype=MEASUREMENT_DTYPE, count=n).copy()
+
+
+MEASUREMENT_DTYPE = np.dtype([
+    ("t_base_ms", "f8"), ("t_opt_ms", "f8"), ("digest_base", "u8"), ("digest_opt", "u8"),
+    ("mismatches", "i8"), ("alg_bytes", "f8"), ("alg_flops", "f8"), ("t_fill_ms", "f8"),
+    ("status", "i4"), ("kernel_id", "i4"), ("launches", "i4"), ("nstages", "i4"),
+])
+
+
+def measure_instances(instances, dev=DEFAULT_DEVICE, **kw) -> list[Measurement]:
+    """Run, time and verify both variants of every instance on the current GPU."""
+    return _convert(instances, measure_raw(list(instances), dev, **kw))
+
+
+def measure_instances_host(instances, in_arrays, in2_arrays, dev=DEFAULT_DEVICE, *, out_base=None,
+                           out_opt=None, skip_opt: bool = False) -> list[Measurement]:
+    """End-to-end variant: instance i's inputs come from host arrays (ideally
+    pinned) and are copied to the device inside the timed batch; outputs are
+    optionally copied back into ``out_base[i]`` / ``out_opt[i]``."""
+    n = len(instances)
+    vp = ctypes.c_void_p
+    keep = []
+
+    def ptrs(arrs, writable=False):
+        if arrs is None:
+            return None
+        a = (vp * max(n, 1))()
+        for k, x in enumerate(arrs):
+            if x is None:
+                a[k] = None
+                continue
+            if hasattr(x, "data_ptr"):
+                a[k] = x.data_ptr()
+            else:
+                x = np.ascontiguousarray(x, dtype=np.float32) if not writable else x
+                keep.append(x)
+                a[k] = x.ctypes.data
+        return a
+
+    rows = (ctypes.c_int64 * max(n, 1))(*[int(x.shape[0]) for x in in_arrays])
+    cols = (ctypes.c_int64 * max(n, 1))(*[int(x.shape[1]) for x in in_arrays])
+    arr = to_c_array(instances)
+    out = (CMeasurement * max(n, 1))()
+    flags = MEASURE_SKIP_OPT if skip_opt else 0
+    rc = lib().lmt_measure_batch_host(arr, n, ctypes.byref(c_device(dev)), flags, ptrs(in_arrays), rows, cols,
+                                      ptrs(in2_arrays), ptrs(out_base, True), ptrs(out_opt, True), out)
+    check(rc, what="measure_batch_host")
+    return _convert(instances, out[:n])
+
+
+def error_of(m: Measurement) -> str:
+    return STATUS_NAMES.get(m.status, f"status {m.status}")
+
+
+__all__ = ["Measurement", "measure_instances", "measure_instances_host", "measure_raw", "last_error"]

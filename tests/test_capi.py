@@ -1,0 +1,55 @@
+"""The C-ABI library loads (no GPU needed) and exports every symbol that
+include/lmt_b200.h declares; the Python binding covers all of them."""
+
+import ctypes
+import os
+import re
+
+from conftest import ROOT
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "lmt_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(lmt_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_header_symbols():
+    from paper_1412_6986_b200 import _lib
+
+    L = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 14
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(names) == set(_lib.EXPORTS)
+
+
+def test_version_and_validation_without_gpu():
+    from paper_1412_6986_b200 import _lib
+
+    assert b"sm_100a" in _lib.lib().lmt_version()
+    rec = _lib.CInstance(64, 64, 32, 32, 0, 2, 2, 0, 1, 3, 2, 1, 1, 1, 1, 16, 16, 8, 8)
+    buf = ctypes.create_string_buffer(512)
+    n = _lib.lib().lmt_validate(ctypes.byref(rec), buf, 512)
+    assert n == 1 and buf.value == b"grid size 256 < 512"
+
+
+def test_struct_layouts_match_header():
+    from paper_1412_6986_b200 import _lib
+
+    assert ctypes.sizeof(_lib.CInstance) == 19 * 4
+    assert ctypes.sizeof(_lib.CDevice) == 10 * 4
+    assert ctypes.sizeof(_lib.CMeasurement) == 8 * 8 + 4 * 4
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    import pytest
+
+    from paper_1412_6986_b200 import _lib
+    from paper_1412_6986_b200.errors import LmtuneError
+
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(LmtuneError, match="no CPU fallback"):
+        _lib.lib()

@@ -1,0 +1,169 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden vectors
+of the reference and against the CPU oracle. Bit-exact for every fp32 output
+(+-inf included), bit-exact fp64 RF means, bit-identical predictions."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1412_6986_b200 as L
+from conftest import GOLDEN_DIR, make_instance
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def test_fill_matches_hash_kat(golden):
+    h = golden["hash"]
+    for salt, key in ((0, "salt0"), (1, "salt1")):
+        n = max(h["idx"]) + 1
+        t = L.interp.device_fill(1, n, salt)[0, :n].cpu().numpy()
+        for i, v in zip(h["idx"], h[key]):
+            assert t[i] == np.float32(v)
+        assert np.array_equal(t, oracle.hash_fill(n, salt))
+
+
+def test_make_inputs_match_reference(golden):
+    for r in golden["interp"][:40]:
+        a, b = L.make_inputs(make_instance(r))
+        assert oracle.out_hash(a) == int(r["in_digest"]) and oracle.out_hash(b) == int(r["in2_digest"])
+
+
+def test_run_pair_matches_reference_all_cases(golden):
+    keep = np.load(f"{GOLDEN_DIR}/interp_outputs.npz")
+    bad = []
+    for k, r in enumerate(golden["interp"]):
+        base, opt = L.run_pair(make_instance(r))
+        if oracle.out_hash(base) != int(r["digest"]) or not np.array_equal(base, opt):
+            bad.append((k, r["pattern"], r["shape"], r["radius"], oracle.out_hash(base) == int(r["digest"])))
+        if f"out{k}" in keep:
+            assert np.array_equal(base, keep[f"out{k}"])
+    assert not bad, bad
+
+
+def test_inf_cases_present_and_exact(golden):
+    inf_cases = [r for r in golden["interp"] if r["n_inf"] > 0]
+    assert inf_cases, "golden set must include +-inf producing chains"
+    for r in inf_cases:
+        base, opt = L.run_pair(make_instance(r))
+        assert oracle.out_hash(base) == int(r["digest"])
+        assert np.isinf(base).sum() == r["n_inf"]
+
+
+def test_execute_accepts_reference_inputs(golden):
+    # execute with inputs of a *different* (larger) instance, like
+    # test_interp.py:121-130 does
+    r = golden["interp"][5]
+    inst = make_instance(r)
+    in_arr, in2 = oracle.make_inputs(inst)
+    big = np.pad(in_arr, ((0, 3), (0, 5)))
+    for v in (L.Variant.BASELINE, L.Variant.OPTIMIZED):
+        got = L.execute(inst, v, big, in2)
+        want = oracle.execute(inst, 0, big, in2)
+        assert np.array_equal(got, want)
+
+
+def test_cfg1_matches_reference(golden):
+    r = golden["cfg1"]
+    base, opt = L.run_pair(make_instance(r))
+    assert oracle.out_hash(base) == int(r["digest"])
+    assert np.array_equal(base, opt)
+
+
+def test_measure_digests_match_oracle(golden):
+    cases = [make_instance(r) for r in golden["interp"][::3]]
+    ms = L.measure_instances(cases)
+    for m, r in zip(ms, golden["interp"][::3]):
+        assert m.status == 0, (m.status, L.measure.last_error())
+        assert m.verified and m.mismatches == 0
+        assert m.digest_base == int(r["digest"]) == m.digest_opt
+        assert m.t_base_ms > 0 and m.t_opt_ms > 0
+
+
+def test_invalid_and_infeasible_are_reported():
+    P, S = L.HomeAccessPattern, L.StencilShape
+    good = L.TemplateParams(2048, 2048, 2048, 2048, P.NO_REUSE_ROW_MAJOR, 8, 8, L.StencilPattern(S.STAR, 0),
+                            5, 1, 0, 0, 0, 0)
+    infeasible = L.KernelInstance(good, L.LaunchConfig(2048, 2048, 32, 32))
+    invalid = L.KernelInstance(good, L.LaunchConfig(16, 16, 8, 8))
+    ms = L.measure_instances([invalid, infeasible])
+    assert ms[0].status == 1 and ms[0].t_opt_ms is None
+    assert ms[1].status == 2 and ms[1].t_opt_ms is None and ms[1].t_base_ms > 0 and ms[1].speedup == 0.0
+    with pytest.raises(L.InvalidInstance):
+        L.run_pair(invalid)
+
+
+def _sample_check(inst, wg_count=3):
+    """Full-size instance: base == opt bitwise everywhere, and the first
+    workgroups match the oracle (size-independent spot check)."""
+    import torch
+
+    geo = L.emit_geometry(inst)
+    p = inst.params
+    a = L.interp.device_fill(geo.alloc_h, geo.alloc_w, 0)
+    b = L.interp.device_fill(p.in_h, p.in_w, 1)
+    base = L.interp.execute_device(inst, L.Variant.BASELINE, a[:, : geo.alloc_w], b[:, : p.in_w])
+    opt = L.interp.execute_device(inst, L.Variant.OPTIMIZED, a[:, : geo.alloc_w], b[:, : p.in_w])
+    assert torch.equal(base.view(torch.int32), opt.view(torch.int32))
+    in_h = a[:, : geo.alloc_w].cpu().numpy()
+    want = oracle.execute(inst, 0, in_h, b[:, : p.in_w].cpu().numpy(), wg_range=(0, wg_count))
+    done = ~np.isnan(want)
+    got = base.cpu().numpy()
+    assert np.array_equal(got[done], want[done])
+
+
+def test_full_size_sweep_instances():
+    tab = L.select_instance_table(L.SamplingSpec(max_instances=20000, seed=0))
+    rng = np.random.default_rng(5)
+    rows = rng.choice(len(tab), size=40, replace=False)
+    cost = L.sweep.estimated_cost(tab.records(rows))
+    for r, c in zip(rows, cost):
+        inst = tab.instance(int(r))
+        if c > 0.5 or L.footprint(inst).bytes > 48 * 1024:
+            continue
+        _sample_check(inst)
+
+
+def test_forest_mean_bitwise():
+    f = L.load(f"{GOLDEN_DIR}/forest_small.txt")
+    ev = np.load(f"{GOLDEN_DIR}/forest_eval.npz")
+    mean = L.forest.predict_mean(f, ev["X"])
+    assert np.array_equal(mean, ev["mean"])
+    pred = L.predict(f, ev["X"])
+    assert np.array_equal(pred, ev["pred"])
+    assert list(L.predict(f, ev["X"][:10])) == [L.predict(f, ev["X"][i]) for i in range(10)]
+    assert np.array_equal(L.decide(f, ev["X"]), ev["pred"] > 1.0)
+
+
+def test_tree_predict_and_votes():
+    f = L.forest.synthetic_forest(ntrees=37, nodes_per_tree=2001, seed=4)  # > 32 trees: two lane chunks
+    X = np.random.default_rng(1).normal(0, 1000, size=(3001, 18))
+    g = L.forest.gpu_forest(f)
+    mean, votes = g.mean(X, votes=True)
+    assert np.array_equal(mean, oracle.forest_mean(f.trees, X))
+    leaves = np.stack([f.trees[t].predict(X) for t in range(3)])
+    for t in range(3):
+        assert np.array_equal(leaves[t], oracle.forest_mean([f.trees[t]], X))
+    want_votes = sum((oracle.forest_mean([t], X) > 0).astype(int) for t in f.trees)
+    assert np.array_equal(votes, want_votes)
+
+
+def test_reference_objects_accepted(lmtune_ref):
+    from lmtune.interp import run_pair as ref_run_pair
+    from lmtune.kernel_model import (HomeAccessPattern, KernelInstance, LaunchConfig, StencilPattern,
+                                     StencilShape, TemplateParams)
+
+    p = TemplateParams(64, 64, 32, 32, HomeAccessPattern.Y_REUSE_COL, 2, 4, StencilPattern(StencilShape.DIAMOND, 2),
+                       3, 2, 1, 1, 1, 1)
+    k = KernelInstance(p, LaunchConfig(32, 32, 4, 8))
+    b, o = L.run_pair(k)
+    rb, ro = ref_run_pair(k)
+    assert np.array_equal(b, rb) and np.array_equal(o, ro)

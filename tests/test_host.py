@@ -1,0 +1,154 @@
+"""Host-side logic of the product (no GPU): geometry, validation, selection,
+sharding and the model-file format, against the reference's golden vectors
+and KATs."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1412_6986_b200 as L
+from conftest import GOLDEN_DIR, make_instance
+
+
+def test_geometry_matches_reference(golden):
+    for r in golden["geometry"]:
+        inst = make_instance(r)
+        g = L.emit_geometry(inst)
+        assert [getattr(g, f) for f in g.__dataclass_fields__] == r["geometry"]
+        fp = L.footprint(inst)
+        assert [fp.row_span, fp.col_span, fp.padded_col_span, fp.bytes] == r["footprint"]
+
+
+def test_validation_messages_match_reference(golden):
+    for r in golden["invalid"]:
+        assert L.validate_instance(make_instance(r)) == r["violations"]
+    for r in golden["interp"][:20]:
+        assert L.validate_instance(make_instance(r)) == []
+
+
+def test_codegen_kats():
+    P, S = L.HomeAccessPattern, L.StencilShape
+
+    def inst(pattern=P.XY_REUSE, n=8, m=8, radius=1, launch=L.LaunchConfig(512, 512, 16, 16)):
+        p = L.TemplateParams(2048, 2048, 2048, 2048, pattern, n, m, L.StencilPattern(S.RECTANGULAR, radius),
+                             10, 10, 2, 2, 1, 1)
+        return L.KernelInstance(p, launch)
+
+    # test_codegen.py:112-127
+    g = L.emit_geometry(inst(n=32, m=32, radius=0))
+    assert (g.num_segs, g.num_warps, g.seg_elems, g.segs_per_row) == (32, 8, 32, 1)
+    g = L.emit_geometry(inst(n=4, m=4, radius=0))
+    assert (g.r_rows, g.r_cols_pad) == (4, 4)
+    with pytest.raises(L.OptimizationInfeasible, match="exceeds capacity"):
+        L.geometry.check_optimizable(inst(P.NO_REUSE_ROW_MAJOR, n=8, m=8, radius=0))
+    # test_codegen.py:172-185 and copy_transaction_count KATs (150-160)
+    assert L.mad_constants(0) == (2.0, 1 / 64)
+    assert L.mad_constants(1) == (0.5, -2 / 64)
+    assert L.mad_constants(3) == (0.5, -0.0625)
+    assert L.mad_constants(5) == (0.5, -1 / 64)
+    assert L.copy_transaction_count(L.Footprint(32, 32, 32, 4096)) == 32
+    assert L.copy_transaction_count(L.Footprint(34, 34, 64, 8704)) == 68
+    assert L.copy_transaction_count(L.Footprint(5, 3, 4, 80)) == 5
+
+
+def test_work_unit_map_kat():
+    # test_kernel_model.py:35-44 (wu_x = 99 example) and bijection
+    p = L.TemplateParams(64, 64, 256, 256, L.HomeAccessPattern.XY_REUSE, 1, 1,
+                         L.StencilPattern(L.StencilShape.STAR, 0), 0, 0, 0, 0, 0, 0)
+    lc = L.LaunchConfig(64, 64, 16, 16)
+    seen = set()
+    for gy in range(4):
+        for gx in range(4):
+            for iy in range(4):
+                for ix in range(4):
+                    for wy in (0, 15):
+                        for wx in (0, 3, 15):
+                            c = L.work_unit_for(lc, p, L.Coord(gy, gx), L.Coord(wy, wx), L.Coord(iy, ix))
+                            assert c not in seen
+                            seen.add(c)
+    c = L.work_unit_for(lc, p, L.Coord(0, 1), L.Coord(0, 3), L.Coord(0, 1))
+    assert c.col == 1 * 16 * 4 + 1 * 16 + 3 == 83
+
+
+def test_selection_matches_reference(golden):
+    for cap, want in golden["selection"].items():
+        tab = L.select_instance_table(L.SamplingSpec(max_instances=int(cap), seed=0))
+        keys = "\n".join(L.instance_key(i) for i in tab.instances())
+        assert len(tab) == want["n"]
+        assert hashlib.sha256(keys.encode()).hexdigest() == want["sha256"]
+
+
+def test_launch_sweep_size():
+    # test_dataset.py:112-128: 4,224 launch configurations at out 2048^2
+    assert len(L.sweep.launch_configs(2048, 2048)) == 4224
+
+
+def test_records_roundtrip():
+    tab = L.select_instance_table(L.SamplingSpec(max_instances=500, seed=3))
+    rec = tab.records()
+    arr = L.kernel_model.to_c_array(tab.instances())
+    import ctypes
+
+    raw = np.frombuffer(bytes(memoryview(arr))[: rec.nbytes], dtype=np.int32).reshape(rec.shape)
+    assert np.array_equal(raw, rec)
+
+
+def test_sharding_is_disjoint_and_balanced():
+    tab = L.select_instance_table(L.SamplingSpec(max_instances=5000, seed=0))
+    cost = L.sweep.estimated_cost(tab.records())
+    for world in (1, 2, 4, 8):
+        for shards in (L.sweep.shard_balanced(cost, world), L.sweep.shard_contiguous(cost, world)):
+            allrows = np.concatenate(shards)
+            assert len(allrows) == len(tab) and len(np.unique(allrows)) == len(tab)
+        loads = [cost[s].sum() for s in L.sweep.shard_balanced(cost, world)]
+        assert max(loads) <= 1.05 * cost.sum() / world + cost.max()
+
+
+def test_model_file_roundtrip(tmp_path):
+    f = L.load(f"{GOLDEN_DIR}/forest_small.txt")
+    assert f.hyperparams == L.Hyperparams(num_trees=20, features_per_node=4, seed=3)
+    p = tmp_path / "m.txt"
+    L.save(f, p)
+    assert p.read_text() == open(f"{GOLDEN_DIR}/forest_small.txt").read()
+
+
+def test_model_file_errors_name_the_line(tmp_path):
+    good = open(f"{GOLDEN_DIR}/forest_small.txt").read().splitlines()
+    bad = tmp_path / "bad.txt"
+    bad.write_text("not-a-model 9\n")
+    with pytest.raises(L.ModelFormatError, match="line 1"):
+        L.load(bad)
+    bad.write_text("\n".join(good[:4]) + "\n")
+    with pytest.raises(L.ModelFormatError, match="unexpected end of file"):
+        L.load(bad)
+    lines = list(good)
+    lines[1] = "num_trees many"
+    bad.write_text("\n".join(lines) + "\n")
+    with pytest.raises(L.ModelFormatError, match="line 2"):
+        L.load(bad)
+    lines = list(good)
+    lines[8] = "feature_names a,b,c"
+    bad.write_text("\n".join(lines) + "\n")
+    with pytest.raises(L.ModelFormatError, match="line 9"):
+        L.load(bad)
+    first = next(ln for ln in good if ln.startswith("node "))
+    bad.write_text("\n".join(good).replace(first, "node 18" + first[len(first.split()[0]) + 1 + len(first.split()[1]):], 1) + "\n")
+    with pytest.raises(L.ModelFormatError, match="feature index 18 out of range"):
+        L.load(bad)
+
+
+def test_reference_forest_load_agrees(lmtune_ref):
+    from lmtune.forest import load as ref_load
+
+    a = ref_load(f"{GOLDEN_DIR}/forest_small.txt")
+    b = L.load(f"{GOLDEN_DIR}/forest_small.txt")
+    for ta, tb in zip(a.trees, b.trees):
+        for f in ("feature", "threshold", "left", "right", "value"):
+            assert np.array_equal(getattr(ta, f), getattr(tb, f))
+
+
+def test_speedup_to_target():
+    assert L.speedup_to_target(1.0) == 0.0
+    assert L.speedup_to_target(8.0) == 3.0
+    assert L.speedup_to_target(0.0) == -10.0
