@@ -9,8 +9,10 @@
  *
  * Conventions
  *  - plain pointers and sizes; no torch types. "d_" pointers are device
- *    memory, "h_" pointers host memory. `stream` is a cudaStream_t (NULL =
- *    the library's own stream for the calling device).
+ *    memory, "h_" pointers host memory. `stream` is a cudaStream_t taken as
+ *    is (NULL = the legacy default stream, as in the CUDA runtime); the
+ *    batch entry points (lmt_measure_batch*) run on the library's own
+ *    stream, see lmt_get_stream().
  *  - every function returns LMT_OK (0) or an LMT_ERR_* code; the message of
  *    the last failure on the calling thread is in lmt_last_error().
  *    LMT_ERR_INVALID_INSTANCE maps to lmtune.errors.InvalidInstance

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -401,7 +402,8 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     // TMA staging geometry: only the `col_span` columns are read
     // (interp.py:94-97 bounds the reads by r_rows x r_cols_pad, and the
     // footprint bounding box guarantees < col_span).
-    const int64_t rows = g.r_rows, cols = g.r_cols;
+    // +3 columns: the box x is aligned down to 16 bytes (see stage_region)
+    const int64_t rows = g.r_rows, cols = g.r_cols + 3;
     int64_t bw, ncc;
     if (round_up(cols, 4) <= 256) {
         bw = round_up(cols, 4);
@@ -434,6 +436,10 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     if (S < 2 && 2 * (int64_t)A.stage_bytes <= smem_cap) S = 2;
     S = std::max<int64_t>(1, std::min<int64_t>(S, nit));
     while (S > 1 && S * (int64_t)A.stage_bytes > smem_cap) S--;
+    if (const char *fs = getenv("LMT_FORCE_STAGES")) {  // debugging aid
+        const int64_t f = atoi(fs);
+        if (f >= 1 && f <= kMaxStages && f * (int64_t)A.stage_bytes <= smem_cap) S = std::min<int64_t>(f, std::max<int64_t>(1, nit));
+    }
     A.nstages = (int32_t)S;
     pl->dyn_smem = (size_t)S * A.stage_bytes;
     if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
@@ -525,7 +531,7 @@ int lmt_fill(float *d_dst, int64_t rows, int64_t cols, int64_t pitch, uint32_t s
     DevCtx *c;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    return launch_fill(d_dst, rows, cols, pitch, salt, stream ? (cudaStream_t)stream : c->stream, c->sms);
+    return launch_fill(d_dst, rows, cols, pitch, salt, (cudaStream_t)stream, c->sms);
 }
 
 int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, const float *d_in, int64_t in_rows,
@@ -549,7 +555,7 @@ int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, co
         return fail(LMT_ERR_INFEASIBLE, "local-memory footprint %lld bytes exceeds capacity %d",
                     (long long)pl.g.footprint_bytes, (int)c->smem_optin - 1024);
     return launch_variant(pl, variant, d_in, in_rows, in_cols, in_pitch, d_in2, d_out,
-                          stream ? (cudaStream_t)stream : c->stream);
+                          (cudaStream_t)stream);
 }
 
 int lmt_digest(const float *d, int64_t count, uint64_t *h_out, void *stream) {
@@ -558,7 +564,7 @@ int lmt_digest(const float *d, int64_t count, uint64_t *h_out, void *stream) {
     DevCtx *c;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    cudaStream_t s = (cudaStream_t)stream;
     rc = ensure(&c->dres, &c->dres_cap, 3);
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(c->dres, 0, 3 * sizeof(unsigned long long), s));
@@ -848,7 +854,7 @@ int lmt_rf_mean(const lmt_forest *f, const double *d_X, int64_t nrows, double *d
         int rc = get_ctx(&c);
         if (rc) return rc;
     }
-    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    cudaStream_t s = (cudaStream_t)stream;
     const int64_t warps = (nrows + 0);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)c->sms * 8));
     const size_t smem = (size_t)f->ncached * sizeof(RfNode);

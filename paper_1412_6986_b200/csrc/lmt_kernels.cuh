@@ -266,15 +266,27 @@ __device__ __forceinline__ void stage_region(const SynthArgs &A, const CUtensorM
     const int ix = it % A.nwx, iy = it / A.nwx;
     const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
     const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
-    // region origin (codegen.py:291-295) shifted into the PAD-ed `in` frame
+    // region origin (codegen.py:291-295) shifted into the PAD-ed `in` frame.
+    // The innermost TMA box coordinate must be 16-byte aligned (measured on
+    // B200: an unaligned x raises an illegal-instruction fault), so the box
+    // starts at org_col rounded down to 4 floats and the region sits at
+    // column (org_col & 3) of the staged rows (see region_shift()).
     const int org_row = A.a[0] * wu_x0 + A.a[1] * wu_y0 + A.off_min_row + A.pad;
-    const int org_col = A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad;
+    const int org_col = (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & ~3;
     float *dst = smem + slot * A.stage_floats;
     mbar_expect_tx(&full[slot], A.stage_bytes);
     for (int cc = 0; cc < A.ncc; ++cc)
         for (int rc = 0; rc < A.nrc; ++rc)
             tma_load_2d(dst + (cc * A.nrc + rc) * A.bh * A.bw, map, &full[slot], org_col + cc * A.bw,
                         org_row + rc * A.bh);
+}
+
+// Column of the staged rows where region column 0 landed for iteration it.
+__device__ __forceinline__ int region_shift(const SynthArgs &A, int it) {
+    const int ix = it % A.nwx, iy = it / A.nwx;
+    const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
+    const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
+    return (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & 3;
 }
 
 template <int SHAPE, int R, bool WIDE>
@@ -326,12 +338,13 @@ __global__ void __launch_bounds__(1024)
         }
         mbar_wait(&full[slot], (it / S) & 1);
         const float *region = smem + slot * A.stage_floats;
+        const int sh = region_shift(A, it);
         float acc;
         if constexpr (WIDE) {
             const SmemWideSrc src{region, A.nrc * A.bh * 256, 0, 0};
-            acc = work_unit<SHAPE, R>(A, src, hr0, hc0, in2c, in2u);
+            acc = work_unit<SHAPE, R>(A, src, hr0, hc0 + sh, in2c, in2u);
         } else {
-            const SmemSrc src{region, A.bw};
+            const SmemSrc src{region + sh, A.bw};
             acc = work_unit<SHAPE, R>(A, src, hr0, hc0, in2c, in2u);
         }
         const int ix = it % A.nwx, iy = it / A.nwx;
