@@ -10,14 +10,15 @@ entry point for TMA descriptors is resolved at run time
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "lmt_capi.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "lmt_kernels.cuh"),
-        os.path.join(os.path.dirname(HERE), "include", "lmt_b200.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu*"))) + [
+    os.path.join(os.path.dirname(HERE), "include", "lmt_b200.h")]
 OUT = os.path.join(HERE, "lib", "liblmt_b200.so")
 
 NVCC_FLAGS = [

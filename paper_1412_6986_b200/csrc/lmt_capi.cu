@@ -16,6 +16,7 @@
 
 #include "../../include/lmt_b200.h"
 #include "lmt_kernels.cuh"
+#include "lmt_synth_ilp.cuh"
 
 #ifndef LMT_VERSION
 #define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
@@ -204,6 +205,19 @@ const KernelSet kKernels[7] = {
     {k_synth_base<-1, -1>, k_synth_opt<-1, -1, false>, k_synth_opt<-1, -1, true>},
 };
 
+// Grouped (ILP) kernels for the compile-time stencils, U = 1, 2, 4.
+struct KernelSetG {
+    BaseFn base[3];
+    OptFn opt[3];
+};
+#define LMT_G(SH, RR)                                                                                  \
+    {{k_synth_base_g<SH, RR, 1>, k_synth_base_g<SH, RR, 2>, k_synth_base_g<SH, RR, 4>},                \
+     {k_synth_opt_g<SH, RR, 1>, k_synth_opt_g<SH, RR, 2>, k_synth_opt_g<SH, RR, 4>}}
+const KernelSetG kKernelsG[6] = {LMT_G(0, 0), LMT_G(2, 1), LMT_G(2, 2), LMT_G(1, 2), LMT_G(0, 1), LMT_G(0, 2)};
+#undef LMT_G
+
+int u_index(int U) { return U == 4 ? 2 : (U == 2 ? 1 : 0); }
+
 int stencil_id(int shape, int r) {
     if (r == 0) return 0;
     if (r == 1) return shape == 0 ? 4 : 1;
@@ -264,6 +278,10 @@ int get_ctx(DevCtx **out) {
             CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt_wide),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
         }
+        for (auto &k : kKernelsG)
+            for (int u = 0; u < 3; u++)
+                CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt[u]),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_rf_mean),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
         c.attrs_set = true;
@@ -289,6 +307,7 @@ struct Plan {
     lmt_geometry g;
     SynthArgs A;
     int sid;
+    int u_base, u_opt;  // work units per thread in lockstep (ILP); 0 = legacy U=1 kernels
     bool feasible;      // footprint <= lmem cap (codegen.py:351)
     bool wide;
     size_t dyn_smem;
@@ -297,6 +316,8 @@ struct Plan {
 };
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+int64_t in2_pitch(int64_t w) { return round_up(w + kIn2HaloCols, 4); }
+size_t in2_phys_elems(int64_t h, int64_t w) { return (size_t)(h + kIn2HaloRows) * (size_t)in2_pitch(w); }
 
 // |U_in2|: union of the in2 cells the context reads touch.
 double in2_union(const lmt_instance &p) {
@@ -440,6 +461,34 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
         const int64_t f = atoi(fs);
         if (f >= 1 && f <= kMaxStages && f * (int64_t)A.stage_bytes <= smem_cap) S = std::min<int64_t>(f, std::max<int64_t>(1, nit));
     }
+    // ILP: few resident warps -> several work units per thread in lockstep
+    const int64_t wgs = (int64_t)p.wg_x * p.wg_y;
+    const double per_smsp = (double)(ctas * warps) / (double)(sms * 4);
+    int U = per_smsp < 2.0 ? 4 : (per_smsp < 4.0 ? 2 : 1);
+    while (U > 1 && (wgs > bound_threads(U, K) || U > nit)) U >>= 1;
+    if (const char *fu = getenv("LMT_FORCE_U")) {  // debugging / tuning aid
+        const int f = atoi(fu);
+        if ((f == 1 || f == 2 || f == 4) && wgs <= bound_threads(f, K)) U = f;
+    }
+    const bool grouped = pl->sid < 6 && !pl->wide;
+    pl->u_base = grouped ? U : 0;
+    if (grouped) {
+        // grouped K2 keeps up to 8 regions in flight; a group needs U slots, overlap needs 2U
+        int64_t S8 = std::max<int64_t>(1, std::min<int64_t>(kMaxStagesG, budget / std::max<int64_t>(1, A.stage_bytes)));
+        while (S8 > 1 && S8 * (int64_t)A.stage_bytes > smem_cap) S8--;
+        int Uo = U;
+        while (Uo > 1 && 2 * Uo > S8) Uo >>= 1;
+        S8 = std::max<int64_t>(1, std::min<int64_t>(S8, std::max<int64_t>(nit, 1)));
+        if (S8 < 2 && nit > 1 && 2 * (int64_t)A.stage_bytes <= smem_cap) S8 = 2;
+        if (const char *fs = getenv("LMT_FORCE_STAGES")) {
+            const int64_t f = atoi(fs);
+            if (f >= Uo && f <= kMaxStagesG && f * (int64_t)A.stage_bytes <= smem_cap) S8 = f;
+        }
+        S = S8;
+        pl->u_opt = Uo;
+    } else {
+        pl->u_opt = 0;
+    }
     A.nstages = (int32_t)S;
     pl->dyn_smem = (size_t)S * A.stage_bytes;
     if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
@@ -464,21 +513,38 @@ int encode_tmap(CUtensorMap *map, const float *d_in, int64_t rows, int64_t cols,
     return LMT_OK;
 }
 
+// d_in2x: in2 in the wrapped-halo layout (k_in2_halo), pitch in2_pitch(in_w)
 int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_rows, int64_t in_cols, int64_t pitch,
-                   const float *d_in2, float *d_out, cudaStream_t s) {
+                   const float *d_in2x, float *d_out, cudaStream_t s) {
     Plan pl = pl0;
     pl.A.in = d_in;
-    pl.A.in2 = d_in2;
+    pl.A.in2 = d_in2x;
+    pl.A.P2 = (int32_t)in2_pitch(pl.A.W2);
     pl.A.out = d_out;
     const KernelSet &ks = kKernels[pl.sid];
     if (variant == 0) {
-        ks.base<<<pl.grid, pl.block, 0, s>>>(pl.A);
+        if (pl.u_base > 0)
+            kKernelsG[pl.sid].base[u_index(pl.u_base)]<<<pl.grid, pl.block, 0, s>>>(pl.A);
+        else
+            ks.base<<<pl.grid, pl.block, 0, s>>>(pl.A);
     } else {
         CUtensorMap map;
         int rc = encode_tmap(&map, d_in, in_rows, in_cols, pitch, pl);
         if (rc) return rc;
-        (pl.wide ? ks.opt_wide : ks.opt)<<<pl.grid, pl.block, pl.dyn_smem, s>>>(map, pl.A);
+        if (pl.u_opt > 0)
+            kKernelsG[pl.sid].opt[u_index(pl.u_opt)]<<<pl.grid, pl.block, pl.dyn_smem, s>>>(map, pl.A);
+        else
+            (pl.wide ? ks.opt_wide : ks.opt)<<<pl.grid, pl.block, pl.dyn_smem, s>>>(map, pl.A);
     }
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+
+int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int sms) {
+    const int64_t total = (h + kIn2HaloRows) * in2_pitch(w);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8));
+    k_in2_halo<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w));
     CUDA_TRY(cudaGetLastError());
     return LMT_OK;
 }
@@ -554,8 +620,16 @@ int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, co
     if (variant == 1 && (int64_t)pl.A.stage_bytes > (int64_t)c->smem_optin - 1024)
         return fail(LMT_ERR_INFEASIBLE, "local-memory footprint %lld bytes exceeds capacity %d",
                     (long long)pl.g.footprint_bytes, (int)c->smem_optin - 1024);
-    return launch_variant(pl, variant, d_in, in_rows, in_cols, in_pitch, d_in2, d_out,
-                          (cudaStream_t)stream);
+    // stage the caller's in2 into the wrapped-halo layout (stream-ordered scratch)
+    cudaStream_t s = (cudaStream_t)stream;
+    float *x = nullptr;
+    CUDA_TRY(cudaMallocAsync(&x, in2_phys_elems(inst->in_h, inst->in_w) * sizeof(float), s));
+    CUDA_TRY(cudaMemcpy2DAsync(x, (size_t)in2_pitch(inst->in_w) * 4, d_in2, (size_t)inst->in_w * 4,
+                               (size_t)inst->in_w * 4, (size_t)inst->in_h, cudaMemcpyDeviceToDevice, s));
+    rc = launch_in2_halo(x, inst->in_h, inst->in_w, s, c->sms);
+    if (rc == LMT_OK) rc = launch_variant(pl, variant, d_in, in_rows, in_cols, in_pitch, x, d_out, s);
+    CUDA_TRY(cudaFreeAsync(x, s));
+    return rc;
 }
 
 int lmt_digest(const float *d, int64_t count, uint64_t *h_out, void *stream) {
@@ -630,11 +704,12 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         }
         m.alg_bytes = pl.alg_bytes;
         m.alg_flops = pl.alg_flops;
-        m.kernel_id = pl.sid * 2 + (pl.wide ? 1 : 0);
+        m.kernel_id = pl.sid * 100 + (pl.wide ? 50 : 0) + pl.u_base * 10 + pl.u_opt;
         cudaEvent_t *ev = &c->events[(size_t)i * 4];
         // ---- inputs (make_inputs, interp.py:30-38)
         const size_t need_in = (size_t)(rows * pitch), need_out = (size_t)p.out_h * p.out_w;
-        const size_t need_in2 = (size_t)p.in_h * p.in_w;
+        const size_t need_in2 = in2_phys_elems(p.in_h, p.in_w);
+        const int64_t p2 = in2_pitch(p.in_w);
         if (host || c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in) {
             if (need_in > c->in_cap) {
                 CUDA_TRY(cudaStreamSynchronize(s));
@@ -666,12 +741,16 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
             if (rc) return rc;
             if (!filled[(size_t)i]) { CUDA_TRY(cudaEventRecord(ev[3], s)); filled[(size_t)i] = 1; }
             if (host) {
-                CUDA_TRY(cudaMemcpyAsync(c->in2, h_in2[i], need_in2 * 4, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaMemcpy2DAsync(c->in2, (size_t)p2 * 4, h_in2[i], (size_t)p.in_w * 4, (size_t)p.in_w * 4,
+                                           (size_t)p.in_h, cudaMemcpyHostToDevice, s));
             } else {
-                rc = launch_fill(c->in2, p.in_h, p.in_w, p.in_w, 1, s, c->sms);
+                rc = launch_fill(c->in2, p.in_h, p.in_w, p2, 1, s, c->sms);
                 if (rc) return rc;
                 m.launches += 1;
             }
+            rc = launch_in2_halo(c->in2, p.in_h, p.in_w, s, c->sms);
+            if (rc) return rc;
+            m.launches += 1;
             c->in2_h = host ? -1 : p.in_h;
             c->in2_w = host ? -1 : p.in_w;
         }

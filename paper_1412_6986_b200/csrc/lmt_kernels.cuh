@@ -32,6 +32,11 @@
 namespace lmt {
 
 constexpr int kMaxStages = 4;
+// in2 is stored with a wrapped halo: physical [IN2_H + 16][P2 >= IN2_W + 8],
+// cell (r, c) = logical in2[r % IN2_H][c % IN2_W]. A context read
+// (t + k) mod IN2_H / IN2_W with k < 16 / 8 then needs no modulo.
+constexpr int kIn2HaloRows = 16;
+constexpr int kIn2HaloCols = 8;
 constexpr int kMaxGenericOffsets = 128;
 
 struct SynthArgs {
@@ -40,6 +45,7 @@ struct SynthArgs {
     float *out;
     int32_t P;            // physical row pitch of `in`, floats (multiple of 4)
     int32_t H2, W2;       // in2 dims (IN2_H, IN2_W)
+    int32_t P2;           // physical row pitch of in2 (W2 + wrapped halo, see k_in2_halo)
     int32_t out_w, grid_x;
     int32_t N, M, nwx, nwy;
     int32_t comp_q, comp_rem;        // comp_ilb = 10*comp_q + comp_rem
@@ -118,8 +124,8 @@ __device__ __forceinline__ int wrap_add(int base, int k, int mod) {
 // in2c points at column glin % IN2_W, in2u at row glin % IN2_H.
 __device__ __forceinline__ float ctx_reads(float acc, const float *in2c, const float *in2u,
                                            int trow, int tcol, int ncoal, int nuncoal,
-                                           int H2, int W2) {
-    for (int k = 0; k < ncoal; ++k) acc = __fadd_rn(acc, ldg_f(in2c + (size_t)wrap_add(trow, k, H2) * W2));
+                                           int H2, int W2, int P2) {
+    for (int k = 0; k < ncoal; ++k) acc = __fadd_rn(acc, ldg_f(in2c + (size_t)wrap_add(trow, k, H2) * P2));
     for (int k = 0; k < nuncoal; ++k) acc = __fadd_rn(acc, ldg_f(in2u + wrap_add(tcol, k, W2)));
     return acc;
 }
@@ -186,7 +192,7 @@ __device__ __forceinline__ float work_unit(const SynthArgs &A, const Src &src, i
             const auto p = src.at(hr, hc);
             acc = stencil_sum<SHAPE, R>(acc, src, p, A);
             acc = mad_ilb(acc, A.comp_q, A.comp_rem);
-            acc = ctx_reads(acc, in2c, in2u, trow, tcol, A.coal_ilb, A.uncoal_ilb, A.H2, A.W2);
+            acc = ctx_reads(acc, in2c, in2u, trow, tcol, A.coal_ilb, A.uncoal_ilb, A.H2, A.W2, A.P2);
             hr += A.a[3];
             hc += A.a[7];
             trow = (trow + 1 == A.H2) ? 0 : trow + 1;
@@ -194,7 +200,7 @@ __device__ __forceinline__ float work_unit(const SynthArgs &A, const Src &src, i
         }
     }
     acc = mad_ep(acc, A.comp_ep, A.comp_ep_phase);
-    acc = ctx_reads(acc, in2c, in2u, A.ep_row0, A.ep_col0, A.coal_ep, A.uncoal_ep, A.H2, A.W2);
+    acc = ctx_reads(acc, in2c, in2u, A.ep_row0, A.ep_col0, A.coal_ep, A.uncoal_ep, A.H2, A.W2, A.P2);
     return acc;
 }
 
@@ -204,12 +210,12 @@ __device__ __forceinline__ float work_unit(const SynthArgs &A, const Src &src, i
 // workgroup, one thread per workitem, work units blocked across workgroups
 // and cyclic across workitems (kernel_model.py:158-170).
 template <int SHAPE, int R>
-__global__ void __launch_bounds__(1024) k_synth_base(const SynthArgs A) {
+__global__ void __launch_bounds__(1024, 1) k_synth_base(const SynthArgs A) {
     const int wi_x = threadIdx.x, wi_y = threadIdx.y;
     const int wg_w = blockDim.x, wg_h = blockDim.y;
     const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
     const float *in2c = A.in2 + (glin % A.W2);
-    const float *in2u = A.in2 + (size_t)(glin % A.H2) * A.W2;
+    const float *in2u = A.in2 + (size_t)(glin % A.H2) * A.P2;
     const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
     const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
     const GlobalSrc src{A.in + (A.pad * A.P + A.pad), A.P};
@@ -290,7 +296,7 @@ __device__ __forceinline__ int region_shift(const SynthArgs &A, int it) {
 }
 
 template <int SHAPE, int R, bool WIDE>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(1024, 1)
     k_synth_opt(const __grid_constant__ CUtensorMap tmap, const SynthArgs A) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(1024)
 
     const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
     const float *in2c = A.in2 + (glin % A.W2);
-    const float *in2u = A.in2 + (size_t)(glin % A.H2) * A.W2;
+    const float *in2u = A.in2 + (size_t)(glin % A.H2) * A.P2;
     // home coordinate of (i=0, j=0) relative to the region origin is the same
     // for every iteration: (a0*wi_x + a1*wi_y - off_min_row, ...)
     const int hr0 = A.a[0] * wi_x + A.a[1] * wi_y - A.off_min_row;
@@ -378,6 +384,18 @@ __global__ void k_fill(float *__restrict__ dst, int64_t rows, int64_t cols, int6
         o.z = (c + 2 < cols) ? hash_value(base + 2) : 0.0f;
         o.w = (c + 3 < cols) ? hash_value(base + 3) : 0.0f;
         reinterpret_cast<float4 *>(dst)[v] = o;
+    }
+}
+
+// Fill the wrapped halo of a physical in2 buffer from its interior
+// (rows >= H2 or columns in [W2, P2) get interior cell (r % H2, c % W2)).
+__global__ void k_in2_halo(float *__restrict__ buf, int H2, int W2, int P2) {
+    const int64_t rows = (int64_t)H2 + kIn2HaloRows;
+    const int64_t total = rows * P2;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = v / P2, c = v - r * P2;
+        if (r < H2 && c < W2) continue;
+        buf[v] = buf[(r % H2) * P2 + (c % W2)];
     }
 }
 
