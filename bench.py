@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dump", default=None, help="save per-instance records and measurements (npz)")
     return ap.parse_args()
 
 
@@ -272,6 +273,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
     gpu_launches = int(res_all["launches"].sum())
+    if args.dump:
+        np.savez(args.dump if world == 1 else f"{args.dump}.rank{rank}", rows=rows_all,
+                 rec=table.records(rows_all), res=res_all)
 
     # ---- end to end: host (pinned) inputs -> H2D -> K1, K2, digest -> D2H outputs
     e2e = None

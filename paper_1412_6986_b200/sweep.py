@@ -261,6 +261,38 @@ def estimated_cost(records: np.ndarray, fp32_lane_ops_per_s: float = 6.0e13, clo
     return 2.0 * (np.maximum(issue, lat) + 4e-6)
 
 
+def chain_ops(records: np.ndarray) -> np.ndarray:
+    """Dependent fp32 operations in one work unit's accumulator chain:
+    N*M*(K + comp_ilb + coal_ilb + uncoal_ilb) + comp_ep + coal_ep + uncoal_ep
+    (codegen.py:207-237; a MAD is one instruction)."""
+    rec = np.asarray(records, dtype=np.int64)
+    K = np.array([_num_offsets(int(s), int(r)) for s, r in zip(rec[:, 7], rec[:, 8])], dtype=np.int64)
+    return rec[:, 5] * rec[:, 6] * (K + rec[:, 9] + rec[:, 11] + rec[:, 13]) + rec[:, 10] + rec[:, 12] + rec[:, 14]
+
+
+def floor_seconds(records: np.ndarray, clock_hz: float = 1.965e9, sms: int = 148,
+                  lanes_per_sm: int = 128) -> tuple[np.ndarray, np.ndarray]:
+    """Per-variant lower bounds on one launch of each instance, with the
+    workgroup -> CTA, workitem -> thread mapping fixed:
+
+    - chain: a workitem's work units are independent but each is a serial
+      chain of fp32 ops (bit-exact order), so a thread needs at least
+      wus * chain issue cycles even with full ILP across its work units;
+    - issue: every warp slot (partial warps included) issues each op once,
+      over 148 SMs x 128 fp32 lanes.
+
+    Returns (chain_floor_s, issue_floor_s)."""
+    rec = np.asarray(records, dtype=np.int64)
+    chain = chain_ops(rec)
+    grid = rec[:, 15] * rec[:, 16]
+    wg = rec[:, 17] * rec[:, 18]
+    wus = rec[:, 2] * rec[:, 3] // np.maximum(grid, 1)
+    warps = (grid // np.maximum(wg, 1)) * ((wg + 31) // 32)
+    chain_s = wus * chain / clock_hz
+    issue_s = warps * 32.0 * wus * chain / (sms * lanes_per_sm * clock_hz)
+    return chain_s.astype(np.float64), issue_s
+
+
 def shard_balanced(costs: np.ndarray, world: int) -> list[np.ndarray]:
     """Disjoint shards of equal estimated cost (greedy longest-processing-time);
     each shard keeps ascending index order."""
