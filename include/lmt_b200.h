@@ -160,6 +160,19 @@ int lmt_rf_mean_host(const lmt_forest *f, const double *h_X, int64_t nrows, doub
                      int32_t *h_votes);
 void lmt_rf_destroy(lmt_forest *f);
 
+/* Compile (NVRTC, sm_100a) and load every specialised kernel a batch of
+ * instances will launch, using up to nthreads host threads (<= 0: all
+ * cores). The reference compiles each kernel instance from its emitted
+ * source with the instance's #defines (codegen.py:150-182); this is that
+ * step, done once per compile tuple and variant. Optional: the measure and
+ * execute entry points compile on first use. *kernels_out = keys needed. */
+int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
+                int32_t nthreads, int64_t *kernels_out);
+
+/* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
+ * compiles) and the host seconds spent compiling. */
+int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);
+
 /* Synchronise the library stream of the current device. */
 int lmt_sync(void);
 

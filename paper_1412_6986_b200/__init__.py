@@ -46,7 +46,14 @@ from .kernel_model import (
     validate_params,
     work_unit_for,
 )
-from .measure import Measurement, measure_instances, measure_instances_host, measure_records
+from .measure import (
+    Measurement,
+    measure_instances,
+    measure_instances_host,
+    measure_records,
+    prepare_instances,
+    prepare_records,
+)
 from .sweep import (
     CompileTuple,
     InstanceTable,

@@ -78,7 +78,7 @@ EXPORTS = (
     "lmt_version", "lmt_last_error", "lmt_validate", "lmt_emit_geometry", "lmt_fill",
     "lmt_execute", "lmt_measure_batch", "lmt_measure_batch_host", "lmt_digest",
     "lmt_rf_create", "lmt_rf_mean", "lmt_rf_mean_host", "lmt_rf_destroy", "lmt_sync",
-    "lmt_get_stream",
+    "lmt_get_stream", "lmt_prepare", "lmt_jit_stats",
 )
 
 _lib = None
@@ -109,6 +109,8 @@ def _declare(L):
     L.lmt_rf_destroy.restype = None
     L.lmt_sync.argtypes = []
     L.lmt_get_stream.argtypes = [P(vp)]
+    L.lmt_prepare.argtypes = [P(CInstance), c_i64, P(CDevice), c_i32, c_i32, P(c_i64)]
+    L.lmt_jit_stats.argtypes = [P(c_i64), P(ctypes.c_double)]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("lmt_version", "lmt_last_error", "lmt_rf_destroy"):
@@ -163,3 +165,10 @@ def library_stream() -> int:
     s = ctypes.c_void_p()
     check(lib().lmt_get_stream(ctypes.byref(s)), what="get_stream")
     return int(s.value or 0)
+
+
+def jit_stats() -> tuple[int, float]:
+    """(kernels compiled by NVRTC in this process, host seconds spent compiling)."""
+    n, t = ctypes.c_int64(), ctypes.c_double()
+    check(lib().lmt_jit_stats(ctypes.byref(n), ctypes.byref(t)), what="jit_stats")
+    return int(n.value), float(t.value)

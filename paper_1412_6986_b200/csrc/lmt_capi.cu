@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -17,6 +18,7 @@
 #include "../../include/lmt_b200.h"
 #include "lmt_kernels.cuh"
 #include "lmt_synth_ilp.cuh"
+#include "lmt_jit_host.cuh"
 
 #ifndef LMT_VERSION
 #define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
@@ -310,6 +312,8 @@ struct Plan {
     int u_base, u_opt;  // work units per thread in lockstep (ILP); 0 = legacy U=1 kernels
     bool feasible;      // footprint <= lmem cap (codegen.py:351)
     bool wide;
+    bool jit;           // NVRTC-specialised kernels (lmt_jit.cuh) instead of the AOT set
+    JitKey kb, ko;      // their keys (baseline, optimized)
     size_t dyn_smem;
     dim3 grid, block;
     double alg_bytes, alg_flops;
@@ -369,6 +373,83 @@ double in_union(const lmt_instance &p) {
     return (double)H * W + 2.0 * r * (H + W) + 4.0 * (r * (r - 1) / 2);
 }
 
+constexpr int kMaxStagesJ = 8;
+JitCache g_jit;
+
+bool jit_enabled() {
+    const char *e = getenv("LMT_JIT");
+    return !(e && e[0] == '0');
+}
+
+// Work units per thread U, prefetch depth D (and, for the optimized
+// variant, staging slots S) for the specialised kernels. A thread's work
+// units are independent chains, so U of them in lockstep give U-way ILP; D
+// prefetched steps hide load latency; S >= 2U slots let the TMA of the next
+// group overlap the current one. All of them cost registers or shared
+// memory, i.e. resident warps. Score = independent chains per SM
+// sub-partition (capped where the fp32 pipe saturates); ties go to TMA
+// overlap, then the larger U (a step's in2 context loads are shared by its U
+// work units), then the larger D.
+//
+// Register estimate, calibrated on ptxas for the NVRTC kernels
+// (tools/jit_check.py over stencils x U x D x variant): values in flight
+// D * (U*K + coal + uncoal) plus a residual for addresses and loop state.
+int64_t jit_regs(int K, int64_t slot, int U, int D, bool opt) {
+    int64_t resid = 40 + 4 * U + (16 * K) / 10;
+    if (opt) resid = (U >= 2 && D >= 2) ? 100 + 6 * U + K : 45 + 2 * K;
+    return D * slot + resid + 8;
+}
+
+void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_t warps, int64_t nit, int64_t sms,
+                bool opt, int64_t stage_bytes, int64_t smem_cap, int *U_out, int *D_out, int *S_out) {
+    const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
+    double best = -1.0;
+    int bu = 1, bd = 2, bs = 1;  // nothing fits the model: get_nospill() steps down if ptxas spills
+    for (int U : {4, 2, 1}) {
+        if (U > nit) continue;
+        for (int Dd : {3, 2, 1}) {
+            if (opt && Dd > 2) continue;  // shared-memory loads: one step of lookahead covers them
+            const int64_t slot = (int64_t)U * K + p.num_coal_ilb + p.num_uncoal_ilb;
+            const int64_t regs = jit_regs(K, slot, U, Dd, opt);
+            if (regs > regcap) continue;
+            const int64_t rregs = (regs + 7) / 8 * 8;
+            for (int Sx : {2 * U, U}) {
+                if (!opt && Sx != 2 * U) continue;
+                const int64_t S = std::min<int64_t>({(int64_t)Sx, kMaxStagesJ, std::max<int64_t>(nit, 1)});
+                if (opt && (S < U || S * stage_bytes > smem_cap)) continue;
+                int64_t res = std::min<int64_t>(32, 64 / std::max<int64_t>(1, warps));
+                res = std::min<int64_t>(res, 65536 / std::max<int64_t>(1, rregs * warps * 32));
+                if (opt) res = std::min<int64_t>(res, (228 * 1024) / (S * stage_bytes + 1024));
+                res = std::max<int64_t>(res, 1);
+                const int64_t act = std::min<int64_t>(res, (ctas + sms - 1) / sms);
+                const double chains = std::min(16.0, (double)act * (double)warps * U / 4.0);
+                const bool overlap = opt && S >= 2 * U;
+                const double score = chains * 64.0 + (overlap ? 16.0 : 0.0) + U * 2.0 + Dd * (chains < 16.0 ? 4.0 : 0.5);
+                if (score > best) { best = score; bu = U; bd = Dd; bs = (int)S; }
+            }
+        }
+    }
+    if (const char *fu = getenv("LMT_FORCE_U")) {
+        const int f = atoi(fu);
+        if (f == 1 || f == 2 || f == 4) bu = (int)std::min<int64_t>(f, std::max<int64_t>(1, nit));
+    }
+    if (const char *fd = getenv("LMT_FORCE_D")) {
+        const int f = atoi(fd);
+        if (f >= 1 && f <= 4) bd = f;
+    }
+    if (opt) {
+        bs = std::max(bs, bu);
+        while (bs > bu && (int64_t)bs * stage_bytes > smem_cap) bs--;
+        if (const char *fs = getenv("LMT_FORCE_STAGES")) {
+            const int f = atoi(fs);
+            if (f >= bu && f <= kMaxStagesJ && (int64_t)f * stage_bytes <= smem_cap) bs = f;
+        }
+    }
+    *U_out = bu;
+    *D_out = bd;
+    *S_out = bs;
+}
+
 int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan *pl, DevCtx *ctx) {
     std::vector<std::string> v = violations(p);
     if (!v.empty()) {
@@ -385,7 +466,8 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     std::vector<int> dr, dc;
     const int K = stencil_offsets(p.stencil_shape, p.stencil_radius, &dr, &dc);
     pl->sid = stencil_id(p.stencil_shape, p.stencil_radius);
-    if (pl->sid == 6 && K > kMaxGenericOffsets) return fail(LMT_ERR_TOO_LARGE, "stencil has %d > %d points", K, kMaxGenericOffsets);
+    if (pl->sid == 6 && K > kMaxGenericOffsets && !jit_enabled())
+        return fail(LMT_ERR_TOO_LARGE, "stencil has %d > %d points", K, kMaxGenericOffsets);
     SynthArgs &A = pl->A;
     memset(&A, 0, sizeof A);
     A.P = (int32_t)in_pitch;
@@ -414,7 +496,7 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     A.off_min_row = g.off_min_row;
     A.off_min_col = g.off_min_col;
     A.K = K;
-    if (pl->sid == 6)
+    if (pl->sid == 6 && K <= kMaxGenericOffsets)
         for (int k = 0; k < K; k++) { A.sdr[k] = (int8_t)dr[k]; A.sdc[k] = (int8_t)dc[k]; }
     pl->block = dim3(p.wg_x, p.wg_y);
     pl->grid = dim3(p.grid_x / p.wg_x, p.grid_y / p.wg_y);
@@ -489,6 +571,30 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     } else {
         pl->u_opt = 0;
     }
+    // NVRTC-specialised kernels: every stencil, straight-line step bodies
+    pl->jit = jit_enabled();
+    if (pl->jit) {
+        const int64_t maxt = wgs <= 256 ? 256 : (wgs <= 512 ? 512 : 1024);
+        const bool ctxwrap = p.num_coal_ilb > kIn2HaloRows || p.num_coal_ep > kIn2HaloRows ||
+                             p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
+        JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
+                  p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
+                  p.in_h, p.in_w, (int)in2_pitch(p.in_w)};
+        int Ub, Db, Uo, Do, Sb, So;
+        choose_jit(K, p, maxt, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
+        choose_jit(K, p, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
+        S = So;
+        pl->kb = k0;
+        pl->kb.U = Ub;
+        pl->kb.D = Db;
+        pl->ko = k0;
+        pl->ko.U = Uo;
+        pl->ko.D = Do;
+        pl->ko.opt = 1;
+        pl->ko.wide = pl->wide ? 1 : 0;
+        pl->u_base = Ub;
+        pl->u_opt = Uo;
+    }
     A.nstages = (int32_t)S;
     pl->dyn_smem = (size_t)S * A.stage_bytes;
     if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
@@ -522,6 +628,26 @@ int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_r
     pl.A.P2 = (int32_t)in2_pitch(pl.A.W2);
     pl.A.out = d_out;
     const KernelSet &ks = kKernels[pl.sid];
+    if (pl.jit) {
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        CUfunction f;
+        std::string err;
+        int rc = g_jit.get_nospill(dev, variant == 0 ? pl.kb : pl.ko, &f, &err);
+        if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
+        if (variant == 0) {
+            void *args[] = {&pl.A};
+            rc = g_jit.launch(f, pl.grid, pl.block, 0, s, args, &err);
+        } else {
+            CUtensorMap map;
+            rc = encode_tmap(&map, d_in, in_rows, in_cols, pitch, pl);
+            if (rc) return rc;
+            void *args[] = {&map, &pl.A};
+            rc = g_jit.launch(f, pl.grid, pl.block, pl.dyn_smem, s, args, &err);
+        }
+        if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
+        return LMT_OK;
+    }
     if (variant == 0) {
         if (pl.u_base > 0)
             kKernelsG[pl.sid].base[u_index(pl.u_base)]<<<pl.grid, pl.block, 0, s>>>(pl.A);
@@ -704,7 +830,8 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         }
         m.alg_bytes = pl.alg_bytes;
         m.alg_flops = pl.alg_flops;
-        m.kernel_id = pl.sid * 100 + (pl.wide ? 50 : 0) + pl.u_base * 10 + pl.u_opt;
+        m.kernel_id = pl.jit ? 10000 + pl.kb.U * 1000 + pl.kb.D * 100 + pl.ko.U * 10 + pl.ko.D
+                             : pl.sid * 100 + (pl.wide ? 50 : 0) + pl.u_base * 10 + pl.u_opt;
         cudaEvent_t *ev = &c->events[(size_t)i * 4];
         // ---- inputs (make_inputs, interp.py:30-38)
         const size_t need_in = (size_t)(rows * pitch), need_out = (size_t)p.out_h * p.out_w;
@@ -758,7 +885,15 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         if (rc) return rc;
         rc = ensure(&c->outo, &c->outo_cap, need_out);
         if (rc) return rc;
-        // ---- K1, K2 timed with events on the launching stream
+        // ---- K1, K2 timed with events on the launching stream; a kernel not
+        // yet compiled/loaded is resolved first, outside the events
+        if (pl.jit) {
+            std::string err;
+            CUfunction f;
+            int jrc = g_jit.get_nospill(c->device, pl.kb, &f, &err);
+            if (!jrc && !(flags & LMT_MEASURE_SKIP_OPT)) jrc = g_jit.get_nospill(c->device, pl.ko, &f, &err);
+            if (jrc) { m.status = fail(LMT_ERR_CUDA, "%s", err.c_str()); continue; }
+        }
         CUDA_TRY(cudaEventRecord(ev[0], s));
         rc = launch_variant(pl, 0, c->in, rows, cols, pitch, c->in2, c->outb, s);
         if (rc) { m.status = rc; continue; }
@@ -823,6 +958,53 @@ int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_devic
                            lmt_measurement *out) {
     if (!h_in || !in_rows || !in_cols || !h_in2) return fail(LMT_ERR_ARG, "host inputs required");
     return measure_impl(insts, n, dev, flags, h_in, in_rows, in_cols, h_in2, h_out_base, h_out_opt, out);
+}
+
+int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags, int32_t nthreads,
+                int64_t *kernels_out) {
+    if ((!insts && n > 0) || n < 0) return fail(LMT_ERR_ARG, "bad prepare arguments");
+    std::vector<JitKey> keys;
+    int device = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        DevCtx *c;
+        int rc = get_ctx(&c);
+        if (rc) return rc;
+        device = c->device;
+        const lmt_device d = dev_or_default(dev);
+        for (int64_t i = 0; i < n; i++) {
+            const lmt_instance &p = insts[i];
+            if (!violations(p).empty()) continue;
+            lmt_geometry g0;
+            if (compute_geometry(p, d, &g0)) continue;
+            Plan pl;
+            if (make_plan(p, d, round_up(g0.alloc_w, 4), &pl, c) || !pl.jit) continue;
+            keys.push_back(pl.kb);
+            const bool run_opt = !(flags & LMT_MEASURE_SKIP_OPT) &&
+                                 (pl.feasible || ((flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
+                                                  (int64_t)pl.A.stage_bytes <= (int64_t)c->smem_optin - 1024));
+            if (run_opt) keys.push_back(pl.ko);
+        }
+    }
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    std::string err;
+    const int nt = nthreads > 0 ? nthreads : (int)std::max(1u, std::thread::hardware_concurrency());
+    int rc = g_jit.prepare(keys, nt, &err);
+    if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
+    for (const JitKey &k : keys) {  // load the modules now, not inside a timed batch
+        CUfunction f;
+        rc = g_jit.get_nospill(device, k, &f, &err);
+        if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
+    }
+    if (kernels_out) *kernels_out = (int64_t)keys.size();
+    return LMT_OK;
+}
+
+int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds) {
+    if (kernels_compiled) *kernels_compiled = g_jit.compiled();
+    if (compile_seconds) *compile_seconds = g_jit.compile_seconds();
+    return LMT_OK;
 }
 
 int lmt_get_stream(void **stream_out) {

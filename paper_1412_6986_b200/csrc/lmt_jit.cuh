@@ -1,0 +1,500 @@
+// lmt_jit.cuh -- K1/K2 specialised per compile tuple, compiled at run time
+// by NVRTC for sm_100a (see lmt_jit_host.cuh). No system headers: the host
+// prepends lmt_args.h and a block of -D style #defines.
+//
+// Why specialise: the reference emits every kernel instance as OpenCL C with
+// its counts and loop bounds as #defines (codegen.py:150-182) and the inner
+// body fully unrolled (_inner_body 207-224, _epilogue 227-237). Run-time
+// counts force either per-step loops or jump tables around each category of
+// operation; on B200 those compile to compare/branch trees that cost more
+// than the arithmetic (ncu: branch_resolving + no_inst + short_sb ~35% of
+// stall samples in the ahead-of-time kernels). Here the stencil, the six
+// counts, the work units per thread U and the prefetch depth D are
+// compile-time, so one (i, j) step is straight-line code: its loads, then a
+// dependent fp32 chain interleaved across U independent work units.
+//
+// Latency: the loads of step t + D - 1 are issued before the chain of step t
+// consumes its own (a D-slot register ring, the step loop unrolled by D), so
+// global/L2 latency hides behind D - 1 steps of arithmetic even when a
+// workgroup is a single warp.
+//
+// Numerics: identical to lmt_kernels.cuh (see its header): per work unit the
+// order is stencil taps row-major, comp_ilb MADs (k restarting every step),
+// coal_ilb reads, uncoal_ilb reads, then the epilogue; every add is one
+// __fadd_rn, every MAD one __fmaf_rn (exact for c1 in {2, 0.5}).
+//
+// Compile-time parameters (all required):
+//   LMT_SHAPE LMT_R                      stencil (0 rect, 1 diamond, 2 star)
+//   LMT_CI LMT_CE                        num_comp_ilb, num_comp_ep
+//   LMT_NC LMT_NCE LMT_NU LMT_NUE        coal/uncoal ilb/ep counts
+//   LMT_U LMT_D                          work units per thread, prefetch depth
+//   LMT_OPT                              0 baseline (global loads), 1 optimized (TMA -> smem)
+//   LMT_WIDE                             optimized variant with several 256-column TMA chunks
+//   LMT_CTXWRAP                          context counts exceed the in2 halo: reduce indices mod IN2_H/W
+//   LMT_H2 LMT_W2 LMT_P2                 in2 shape (IN2_H, IN2_W: #defines in the reference too) and
+//                                        its physical pitch, so every context read of a step is
+//                                        one base register plus an immediate offset
+
+namespace lmt {
+
+constexpr int SHAPE = LMT_SHAPE, RAD = LMT_R;
+constexpr int CI = LMT_CI, CE = LMT_CE, NC = LMT_NC, NCE = LMT_NCE, NU = LMT_NU, NUE = LMT_NUE;
+constexpr int U = LMT_U, D = LMT_D;
+constexpr int kMaxStagesJ = 8;
+constexpr int H2 = LMT_H2, W2 = LMT_W2, P2 = LMT_P2;
+
+// ----------------------------------------------------- stencil (kernel_model.py:115-130)
+__host__ __device__ constexpr bool tap_in(int a, int b) {
+    return SHAPE == 0 ? true
+         : SHAPE == 1 ? ((a < 0 ? -a : a) + (b < 0 ? -b : b) <= RAD)
+                      : (a == 0 || b == 0);
+}
+__host__ __device__ constexpr int tap_count() {
+    int k = 0;
+    for (int a = -RAD; a <= RAD; ++a)
+        for (int b = -RAD; b <= RAD; ++b)
+            if (tap_in(a, b)) ++k;
+    return k;
+}
+__host__ __device__ constexpr int tap_dr(int idx) {
+    int k = 0;
+    for (int a = -RAD; a <= RAD; ++a)
+        for (int b = -RAD; b <= RAD; ++b)
+            if (tap_in(a, b)) {
+                if (k == idx) return a;
+                ++k;
+            }
+    return 0;
+}
+__host__ __device__ constexpr int tap_dc(int idx) {
+    int k = 0;
+    for (int a = -RAD; a <= RAD; ++a)
+        for (int b = -RAD; b <= RAD; ++b)
+            if (tap_in(a, b)) {
+                if (k == idx) return b;
+                ++k;
+            }
+    return 0;
+}
+constexpr int KT = tap_count();
+
+// ----------------------------------------------------- MAD constants (codegen.py:58-66)
+__host__ __device__ constexpr float mad_c1(int k) { return (k & 1) ? 0.5f : 2.0f; }
+__host__ __device__ constexpr float mad_c2(int k) {
+    return ((k & 1) ? -1.0f : 1.0f) * (float)(1 + k % 5) * (1.0f / 64.0f);
+}
+
+// ----------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct alignas(64) TensorMap {
+    unsigned long long opaque[16];
+};
+
+__device__ __forceinline__ void tma_load_2d(float *dst, const TensorMap *map, unsigned long long *bar, int x,
+                                            int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+// ----------------------------------------------------- target-array sources
+
+// K1: plain global loads through the read-only path.
+struct GlobalSrc {
+    const float *p[U];  // element (home row, home col) of (i=0, j=0), per work unit
+    int pitch;
+    template <int NU_>
+    __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) {
+            const float *q = p[u] + (r * pitch + c);
+#pragma unroll
+            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(q + (tap_dr(k) * pitch + tap_dc(k)));
+        }
+    }
+};
+
+// K2: the staged region, row-major with pitch bw (one TMA column chunk).
+struct SmemSrc {
+    const float *p[U];  // shared-memory element of (i=0, j=0), per work unit
+    int pitch;
+    template <int NU_>
+    __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) {
+            const float *q = p[u] + (r * pitch + c);
+#pragma unroll
+            for (int k = 0; k < KT; ++k) v[u][k] = q[tap_dr(k) * pitch + tap_dc(k)];
+        }
+    }
+};
+
+// K2 with several 256-wide column chunks: smem [ccol][rows_padded][256].
+struct SmemWideSrc {
+    const float *slot[U];  // stage base per work unit
+    int hr[U], hc[U];      // region coordinate of (i=0, j=0) per work unit
+    int chunk;             // rows_padded * 256
+    template <int NU_>
+    __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) {
+#pragma unroll
+            for (int k = 0; k < KT; ++k) {
+                const int row = hr[u] + r + tap_dr(k), col = hc[u] + c + tap_dc(k);
+                v[u][k] = slot[u][(col >> 8) * chunk + row * 256 + (col & 255)];
+            }
+        }
+    }
+};
+
+// ----------------------------------------------------- the step pipeline
+
+constexpr int NCs = NC > 0 ? NC : 1;
+constexpr int NUs = NU > 0 ? NU : 1;
+
+template <int NU_>
+struct Slot {
+    float v[NU_][KT];
+    float c[NCs];
+    float w[NUs];
+};
+
+// Load cursor: the (i, j) step a slot is filled for.
+struct Cursor {
+    int r, c;          // home-coordinate offset of the step from (i=0, j=0)
+    int j;
+    const float *crow; // coal: in2 row trow at column glin % IN2_W
+    int trow;
+    const float *ucol; // uncoal: in2 row glin % IN2_H, column tcol
+    int tcol;
+};
+
+__device__ __forceinline__ float ctx_coal(const SynthArgs &A, const float *in2c, const float *crow, int trow,
+                                          int k) {
+#if LMT_CTXWRAP
+    return __ldg(in2c + (size_t)((trow + k) % H2) * P2);
+#else
+    return __ldg(crow + k * P2);
+#endif
+}
+__device__ __forceinline__ float ctx_uncoal(const SynthArgs &A, const float *in2u, const float *ucol, int tcol,
+                                            int k) {
+#if LMT_CTXWRAP
+    return __ldg(in2u + (tcol + k) % W2);
+#else
+    return __ldg(ucol + k);
+#endif
+}
+
+template <int NU_, class Src>
+__device__ __forceinline__ void fill(Slot<NU_> &s, const Src &src, const Cursor &q, const SynthArgs &A,
+                                     const float *in2c, const float *in2u) {
+    src.template load<NU_>(s.v, q.r, q.c);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) s.c[k] = ctx_coal(A, in2c, q.crow, q.trow, k);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) s.w[k] = ctx_uncoal(A, in2u, q.ucol, q.tcol, k);
+}
+
+__device__ __forceinline__ void advance(Cursor &q, const SynthArgs &A, const float *in2c, const float *in2u) {
+    // j-walk, then the i carriage return (home coordinate affine in i, j)
+    q.r += A.a[3];
+    q.c += A.a[7];
+    if (++q.j == A.M) {
+        q.j = 0;
+        q.r += A.a[2] - A.M * A.a[3];
+        q.c += A.a[6] - A.M * A.a[7];
+    }
+    // (i*M + j) mod IN2_H / IN2_W
+    if (++q.trow == H2) {
+        q.trow = 0;
+        q.crow = in2c;
+    } else {
+        q.crow += P2;
+    }
+    if (++q.tcol == W2) {
+        q.tcol = 0;
+        q.ucol = in2u;
+    } else {
+        q.ucol += 1;
+    }
+}
+
+template <int NU_>
+__device__ __forceinline__ void consume(float (&acc)[NU_], const Slot<NU_> &s) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], s.v[u][k]);
+#pragma unroll
+    for (int k = 0; k < CI; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fmaf_rn(acc[u], mad_c1(k), mad_c2(k));
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], s.c[k]);
+#pragma unroll
+    for (int k = 0; k < NU; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], s.w[k]);
+}
+
+// NU_ work units of one thread: the full i/j nest then the epilogue.
+template <int NU_, class Src>
+__device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, const float *in2c, const float *in2u,
+                                          float (&acc)[NU_]) {
+#pragma unroll
+    for (int u = 0; u < NU_; ++u) acc[u] = 0.0f;
+    const int NM = A.N * A.M;
+    Cursor q{0, 0, 0, in2c, 0, in2u, 0};
+    Slot<NU_> s[D];
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d)
+        if (d < NM) {
+            fill<NU_>(s[d], src, q, A, in2c, in2u);
+            advance(q, A, in2c, in2u);
+        }
+    for (int t0 = 0; t0 < NM; t0 += D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int t = t0 + d;
+            if (t < NM) {
+                if (t + D - 1 < NM) {
+                    fill<NU_>(s[(d + D - 1) % D], src, q, A, in2c, in2u);
+                    advance(q, A, in2c, in2u);
+                }
+                consume<NU_>(acc, s[d]);
+            }
+        }
+    }
+    // epilogue (codegen.py:227-237): loads first, then the chain
+    float ce[NCE > 0 ? NCE : 1], ue[NUE > 0 ? NUE : 1];
+#pragma unroll
+    for (int k = 0; k < NCE; ++k) ce[k] = ctx_coal(A, in2c, in2c + (size_t)A.ep_row0 * P2, A.ep_row0, k);
+#pragma unroll
+    for (int k = 0; k < NUE; ++k) ue[k] = ctx_uncoal(A, in2u, in2u + A.ep_col0, A.ep_col0, k);
+#pragma unroll
+    for (int k = 0; k < CE; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fmaf_rn(acc[u], mad_c1(CI + k), mad_c2(CI + k));
+#pragma unroll
+    for (int k = 0; k < NCE; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], ce[k]);
+#pragma unroll
+    for (int k = 0; k < NUE; ++k)
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], ue[k]);
+}
+
+// ----------------------------------------------------- K1
+
+#if !LMT_OPT
+// blockDim = (WG_W, WG_H), gridDim = (GRID_X/WG_W, GRID_Y/WG_H); work units
+// blocked across workgroups, cyclic across workitems (kernel_model.py:158-170).
+extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const SynthArgs A) {
+    const int wi_x = threadIdx.x, wi_y = threadIdx.y;
+    const int wg_w = blockDim.x, wg_h = blockDim.y;
+    const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
+    const float *in2c = A.in2 + (glin % W2);
+    const float *in2u = A.in2 + (size_t)(glin % H2) * P2;
+    const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
+    const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
+    const float *in0 = A.in + (A.pad * A.P + A.pad);
+    const int nit = A.nwx * A.nwy;
+    int it = 0;
+    for (; it + U <= nit; it += U) {
+        GlobalSrc src;
+        src.pitch = A.P;
+        size_t o[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int ix = (it + u) % A.nwx, iy = (it + u) / A.nwx;
+            const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
+            src.p[u] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
+            o[u] = (size_t)wu_y * A.out_w + wu_x;
+        }
+        float acc[U];
+        run_units<U>(A, src, in2c, in2u, acc);
+#pragma unroll
+        for (int u = 0; u < U; ++u) A.out[o[u]] = acc[u];
+    }
+    for (; it < nit; ++it) {
+        const int ix = it % A.nwx, iy = it / A.nwx;
+        const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
+        GlobalSrc src;
+        src.pitch = A.P;
+        src.p[0] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
+        float acc[1];
+        run_units<1>(A, src, in2c, in2u, acc);
+        A.out[(size_t)wu_y * A.out_w + wu_x] = acc[0];
+    }
+}
+#endif
+
+// ----------------------------------------------------- K2
+
+#if LMT_OPT
+// Stage the region of work-unit iteration `it` into slot `slot` (the
+// cooperative copy of codegen.py:296-311, done by the TMA engine). The
+// innermost box coordinate must be 16-byte aligned, so the box starts at
+// org_col rounded down to 4 floats; region column 0 sits at (org_col & 3).
+__device__ __forceinline__ void stage_region(const SynthArgs &A, const TensorMap *map, float *smem,
+                                             unsigned long long *full, int slot, int it) {
+    const int ix = it % A.nwx, iy = it / A.nwx;
+    const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
+    const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
+    const int org_row = A.a[0] * wu_x0 + A.a[1] * wu_y0 + A.off_min_row + A.pad;
+    const int org_col = (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & ~3;
+    float *dst = smem + slot * A.stage_floats;
+    mbar_expect_tx(&full[slot], A.stage_bytes);
+    for (int cc = 0; cc < A.ncc; ++cc)
+        for (int rc = 0; rc < A.nrc; ++rc)
+            tma_load_2d(dst + (cc * A.nrc + rc) * A.bh * A.bw, map, &full[slot], org_col + cc * A.bw,
+                        org_row + rc * A.bh);
+}
+
+__device__ __forceinline__ int region_shift(const SynthArgs &A, int it) {
+    const int ix = it % A.nwx, iy = it / A.nwx;
+    const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
+    const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
+    return (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & 3;
+}
+
+// Slots: iteration `it` lives in slot it % S; thread 0 re-arms a slot for
+// iteration it + S once every warp released it. With S >= 2U a group's
+// regions are in flight while the previous group computes.
+extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
+    lmt_kernel(const __grid_constant__ TensorMap tmap, const SynthArgs A) {
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) unsigned long long full[kMaxStagesJ], empty[kMaxStagesJ];
+
+    const int wi_x = threadIdx.x, wi_y = threadIdx.y;
+    const int wg_w = blockDim.x, wg_h = blockDim.y;
+    const int tid = wi_y * wg_w + wi_x;
+    const int nwarps = (wg_w * wg_h + 31) >> 5;
+    const int lane = tid & 31;
+    const int S = A.nstages;
+    const int nit = A.nwx * A.nwy;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], nwarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap)) : "memory");
+        for (int s = 0; s < S && s < nit; ++s) stage_region(A, &tmap, smem, full, s, s);
+    }
+    const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
+    const float *in2c = A.in2 + (glin % W2);
+    const float *in2u = A.in2 + (size_t)(glin % H2) * P2;
+    // home coordinate of (i=0, j=0) relative to the region origin: the same
+    // for every iteration (a0*wi_x + a1*wi_y - off_min_row, ...)
+    const int hr0 = A.a[0] * wi_x + A.a[1] * wi_y - A.off_min_row;
+    const int hc0 = A.a[4] * wi_x + A.a[5] * wi_y - A.off_min_col;
+    const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
+    const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
+
+    int prev0 = 0, prevcnt = 0;
+    for (int it0 = 0; it0 < nit;) {
+        const int cnt = (it0 + U <= nit) ? U : 1;
+        if (tid == 0) {  // re-arm the slots the previous group released
+            for (int q = 0; q < prevcnt; ++q) {
+                const int pit = prev0 + q;
+                if (pit + S < nit) {
+                    mbar_wait(&empty[pit % S], (pit / S) & 1);
+                    stage_region(A, &tmap, smem, full, pit % S, pit + S);
+                }
+            }
+        }
+        if (cnt == U) {
+#if LMT_WIDE
+            SmemWideSrc src;
+            src.chunk = A.nrc * A.bh * 256;
+#else
+            SmemSrc src;
+            src.pitch = A.bw;
+#endif
+            size_t o[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int it = it0 + u;
+                mbar_wait(&full[it % S], (it / S) & 1);
+                const float *slot = smem + (it % S) * A.stage_floats;
+#if LMT_WIDE
+                src.slot[u] = slot;
+                src.hr[u] = hr0;
+                src.hc[u] = hc0 + region_shift(A, it);
+#else
+                src.p[u] = slot + region_shift(A, it) + (hr0 * A.bw + hc0);
+#endif
+                const int ix = it % A.nwx, iy = it / A.nwx;
+                o[u] = (size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w);
+            }
+            float acc[U];
+            run_units<U>(A, src, in2c, in2u, acc);
+#pragma unroll
+            for (int u = 0; u < U; ++u) A.out[o[u]] = acc[u];
+        } else {
+            const int it = it0;
+            mbar_wait(&full[it % S], (it / S) & 1);
+            const float *slot = smem + (it % S) * A.stage_floats;
+#if LMT_WIDE
+            SmemWideSrc src;
+            src.chunk = A.nrc * A.bh * 256;
+            src.slot[0] = slot;
+            src.hr[0] = hr0;
+            src.hc[0] = hc0 + region_shift(A, it);
+#else
+            SmemSrc src;
+            src.pitch = A.bw;
+            src.p[0] = slot + region_shift(A, it) + (hr0 * A.bw + hc0);
+#endif
+            float acc[1];
+            run_units<1>(A, src, in2c, in2u, acc);
+            const int ix = it % A.nwx, iy = it / A.nwx;
+            A.out[(size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w)] = acc[0];
+        }
+        __syncwarp();
+        if (lane == 0)
+            for (int q = 0; q < cnt; ++q) mbar_arrive(&empty[(it0 + q) % S]);
+        prev0 = it0;
+        prevcnt = cnt;
+        it0 += cnt;
+    }
+}
+#endif
+
+}  // namespace lmt

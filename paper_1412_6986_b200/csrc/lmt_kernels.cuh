@@ -29,40 +29,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "lmt_args.h"
+
 namespace lmt {
 
 constexpr int kMaxStages = 4;
-// in2 is stored with a wrapped halo: physical [IN2_H + 16][P2 >= IN2_W + 8],
-// cell (r, c) = logical in2[r % IN2_H][c % IN2_W]. A context read
-// (t + k) mod IN2_H / IN2_W with k < 16 / 8 then needs no modulo.
-constexpr int kIn2HaloRows = 16;
-constexpr int kIn2HaloCols = 8;
-constexpr int kMaxGenericOffsets = 128;
-
-struct SynthArgs {
-    const float *in;
-    const float *in2;
-    float *out;
-    int32_t P;            // physical row pitch of `in`, floats (multiple of 4)
-    int32_t H2, W2;       // in2 dims (IN2_H, IN2_W)
-    int32_t P2;           // physical row pitch of in2 (W2 + wrapped halo, see k_in2_halo)
-    int32_t out_w, grid_x;
-    int32_t N, M, nwx, nwy;
-    int32_t comp_q, comp_rem;        // comp_ilb = 10*comp_q + comp_rem
-    int32_t comp_ep, comp_ep_phase;  // epilogue MADs start at k = comp_ilb
-    int32_t coal_ilb, coal_ep, uncoal_ilb, uncoal_ep;
-    int32_t ep_row0, ep_col0;        // (N*M) % IN2_H, (N*M) % IN2_W
-    int32_t a[8];                    // pattern_affine: row_wu_x,row_wu_y,row_i,row_j,col_wu_x,col_wu_y,col_i,col_j
-    int32_t pad;
-    // optimized variant: region origin offsets and TMA staging geometry
-    int32_t off_min_row, off_min_col;
-    int32_t bw, bh, nrc, ncc;        // box width/height, row/col chunk counts
-    int32_t stage_floats, nstages;
-    uint32_t stage_bytes;
-    // generic stencil (radius > 2)
-    int32_t K;
-    int8_t sdr[kMaxGenericOffsets], sdc[kMaxGenericOffsets];
-};
 
 // ---------------------------------------------------------------- helpers
 

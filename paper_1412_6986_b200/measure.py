@@ -116,6 +116,34 @@ def measure_records(records, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allo
     return np.frombuffer(out, dtype=MEASUREMENT_DTYPE, count=n).copy()
 
 
+def prepare_records(records, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False,
+                    nthreads: int = 0) -> int:
+    """Compile (NVRTC, sm_100a) and load every specialised kernel that
+    measuring ``records`` will launch -- the reference's per-kernel compile
+    step (codegen.py:150-182) -- in parallel host threads. Returns the number
+    of distinct kernels the batch needs."""
+    from .sweep import records_to_c
+
+    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    n = len(records)
+    arr = records_to_c(records)
+    out = ctypes.c_int64()
+    check(lib().lmt_prepare(arr, n, ctypes.byref(c_device(dev)), flags, nthreads, ctypes.byref(out)),
+          what="prepare")
+    return int(out.value)
+
+
+def prepare_instances(instances, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False,
+                      nthreads: int = 0) -> int:
+    """prepare_records for KernelInstance objects."""
+    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    instances = list(instances)
+    out = ctypes.c_int64()
+    check(lib().lmt_prepare(to_c_array(instances), len(instances), ctypes.byref(c_device(dev)), flags, nthreads,
+                            ctypes.byref(out)), what="prepare")
+    return int(out.value)
+
+
 MEASUREMENT_DTYPE = np.dtype([
     ("t_base_ms", "f8"), ("t_opt_ms", "f8"), ("digest_base", "u8"), ("digest_opt", "u8"),
     ("mismatches", "i8"), ("alg_bytes", "f8"), ("alg_flops", "f8"), ("t_fill_ms", "f8"),
@@ -168,4 +196,5 @@ def error_of(m: Measurement) -> str:
     return STATUS_NAMES.get(m.status, f"status {m.status}")
 
 
-__all__ = ["Measurement", "measure_instances", "measure_instances_host", "measure_raw", "last_error"]
+__all__ = ["Measurement", "measure_instances", "measure_instances_host", "measure_raw", "prepare_records",
+           "prepare_instances", "last_error"]
