@@ -37,5 +37,11 @@ struct SynthArgs {
 // (t + k) mod IN2_H / IN2_W with k < 16 / 8 then needs no modulo.
 constexpr int kIn2HaloRows = 16;
 constexpr int kIn2HaloCols = 8;
+// The physical halo is wider: the specialised kernels prefetch the in2 lines
+// of the step kPfMax steps ahead into L1 without wrapping the index, so
+// those addresses must stay inside the buffer (they hold wrapped copies too).
+constexpr int kPfMax = 32;
+constexpr int kIn2PhysHaloRows = kIn2HaloRows + kPfMax;
+constexpr int kIn2PhysHaloCols = kIn2HaloCols + kPfMax;
 
 }  // namespace lmt

@@ -320,8 +320,8 @@ struct Plan {
 };
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
-int64_t in2_pitch(int64_t w) { return round_up(w + kIn2HaloCols, 4); }
-size_t in2_phys_elems(int64_t h, int64_t w) { return (size_t)(h + kIn2HaloRows) * (size_t)in2_pitch(w); }
+int64_t in2_pitch(int64_t w) { return round_up(w + kIn2PhysHaloCols, 32); }  // rows start on 128-byte lines
+size_t in2_phys_elems(int64_t h, int64_t w) { return (size_t)(h + kIn2PhysHaloRows) * (size_t)in2_pitch(w); }
 
 // |U_in2|: union of the in2 cells the context reads touch.
 double in2_union(const lmt_instance &p) {
@@ -373,8 +373,14 @@ double in_union(const lmt_instance &p) {
     return (double)H * W + 2.0 * r * (H + W) + 4.0 * (r * (r - 1) / 2);
 }
 
-constexpr int kMaxStagesJ = 8;
+constexpr int kMaxStagesJ = 16;
 JitCache g_jit;
+
+int jit_pf() {
+    const char *e = getenv("LMT_PF");
+    const int v = e ? atoi(e) : 8;
+    return std::max(0, std::min(v, kPfMax - 1));
+}
 
 bool jit_enabled() {
     const char *e = getenv("LMT_JIT");
@@ -382,56 +388,56 @@ bool jit_enabled() {
 }
 
 // Work units per thread U, prefetch depth D (and, for the optimized
-// variant, staging slots S) for the specialised kernels. A thread's work
-// units are independent chains, so U of them in lockstep give U-way ILP; D
-// prefetched steps hide load latency; S >= 2U slots let the TMA of the next
-// group overlap the current one. All of them cost registers or shared
-// memory, i.e. resident warps. Score = independent chains per SM
-// sub-partition (capped where the fp32 pipe saturates); ties go to TMA
-// overlap, then the larger U (a step's in2 context loads are shared by its U
-// work units), then the larger D.
+// variant, staging slots S) for the specialised kernels.
 //
-// Register estimate, calibrated on ptxas for the NVRTC kernels
-// (tools/jit_check.py over stencils x U x D x variant): values in flight
-// D * (U*K + coal + uncoal) plus a residual for addresses and loop state.
-int64_t jit_regs(int K, int64_t slot, int U, int D, bool opt) {
-    int64_t resid = 40 + 4 * U + (16 * K) / 10;
-    if (opt) resid = (U >= 2 && D >= 2) ? 100 + 6 * U + K : 45 + 2 * K;
-    return D * slot + resid + 8;
+// A thread's work units are independent fp32 chains, so U of them in
+// lockstep give U-way ILP, and the in2 context loads of a step are shared by
+// its U work units (U times fewer context loads and L1 wavefronts per chain
+// operation); D prefetched steps hide load latency. Measured on B200
+// (tools/gpu_ud.sh): the largest U and D the register file holds win on
+// every representative launch shape, from one-thread workgroups to 1024-
+// thread ones, so the baseline asks for U = 8, D = 3 and JitCache::resolve
+// steps D, then U, down until ptxas does not spill.
+//
+// The optimized variant also needs S >= U staged regions per CTA (S >= 2U to
+// overlap the next group's TMA with the current group), and shared memory
+// bounds residency: score = independent chains per SM sub-partition, then
+// TMA overlap, then U, then D.
+int64_t jit_regs_guess(int K, int64_t slot, int U, int D) {
+    return std::min<int64_t>(255, D * slot + 100 + 6 * U + K);
 }
 
 void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_t warps, int64_t nit, int64_t sms,
                 bool opt, int64_t stage_bytes, int64_t smem_cap, int *U_out, int *D_out, int *S_out) {
-    const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
-    double best = -1.0;
-    int bu = 1, bd = 2, bs = 1;  // nothing fits the model: get_nospill() steps down if ptxas spills
-    for (int U : {4, 2, 1}) {
-        if (U > nit) continue;
-        for (int Dd : {3, 2, 1}) {
-            if (opt && Dd > 2) continue;  // shared-memory loads: one step of lookahead covers them
+    int bu = 1, bd = 3, bs = 1;
+    for (int U : {8, 4, 2, 1})
+        if (U <= nit) { bu = U; break; }
+    if (opt) {
+        bd = 2;  // shared-memory loads: one step of lookahead covers them
+        double best = -1.0;
+        for (int U : {8, 4, 2, 1}) {
+            if (U > nit) continue;
             const int64_t slot = (int64_t)U * K + p.num_coal_ilb + p.num_uncoal_ilb;
-            const int64_t regs = jit_regs(K, slot, U, Dd, opt);
-            if (regs > regcap) continue;
+            const int64_t regs = std::min<int64_t>(jit_regs_guess(K, slot, U, 2), 65536 / maxt);
             const int64_t rregs = (regs + 7) / 8 * 8;
             for (int Sx : {2 * U, U}) {
-                if (!opt && Sx != 2 * U) continue;
                 const int64_t S = std::min<int64_t>({(int64_t)Sx, kMaxStagesJ, std::max<int64_t>(nit, 1)});
-                if (opt && (S < U || S * stage_bytes > smem_cap)) continue;
+                if (S < U || S * stage_bytes > smem_cap) continue;
                 int64_t res = std::min<int64_t>(32, 64 / std::max<int64_t>(1, warps));
                 res = std::min<int64_t>(res, 65536 / std::max<int64_t>(1, rregs * warps * 32));
-                if (opt) res = std::min<int64_t>(res, (228 * 1024) / (S * stage_bytes + 1024));
+                res = std::min<int64_t>(res, (228 * 1024) / (S * stage_bytes + 1024));
                 res = std::max<int64_t>(res, 1);
                 const int64_t act = std::min<int64_t>(res, (ctas + sms - 1) / sms);
-                const double chains = std::min(16.0, (double)act * (double)warps * U / 4.0);
-                const bool overlap = opt && S >= 2 * U;
-                const double score = chains * 64.0 + (overlap ? 16.0 : 0.0) + U * 2.0 + Dd * (chains < 16.0 ? 4.0 : 0.5);
-                if (score > best) { best = score; bu = U; bd = Dd; bs = (int)S; }
+                const double chains = std::min(64.0, (double)act * (double)warps * U / 4.0);
+                const bool overlap = S >= 2 * U;
+                const double score = chains * 64.0 + (overlap ? 16.0 : 0.0) + U * 2.0;
+                if (score > best) { best = score; bu = U; bs = (int)S; }
             }
         }
     }
     if (const char *fu = getenv("LMT_FORCE_U")) {
         const int f = atoi(fu);
-        if (f == 1 || f == 2 || f == 4) bu = (int)std::min<int64_t>(f, std::max<int64_t>(1, nit));
+        if (f == 1 || f == 2 || f == 4 || f == 8) bu = (int)std::min<int64_t>(f, std::max<int64_t>(1, nit));
     }
     if (const char *fd = getenv("LMT_FORCE_D")) {
         const int f = atoi(fd);
@@ -579,7 +585,7 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
                              p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
         JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
                   p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
-                  p.in_h, p.in_w, (int)in2_pitch(p.in_w)};
+                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf()};
         int Ub, Db, Uo, Do, Sb, So;
         choose_jit(K, p, maxt, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
         choose_jit(K, p, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
@@ -633,7 +639,7 @@ int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_r
         CUDA_TRY(cudaGetDevice(&dev));
         CUfunction f;
         std::string err;
-        int rc = g_jit.get_nospill(dev, variant == 0 ? pl.kb : pl.ko, &f, &err);
+        int rc = g_jit.get(dev, variant == 0 ? pl.kb : pl.ko, &f, nullptr, &err);
         if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
         if (variant == 0) {
             void *args[] = {&pl.A};
@@ -668,7 +674,7 @@ int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_r
 
 
 int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int sms) {
-    const int64_t total = (h + kIn2HaloRows) * in2_pitch(w);
+    const int64_t total = (h + kIn2PhysHaloRows) * in2_pitch(w);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8));
     k_in2_halo<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w));
     CUDA_TRY(cudaGetLastError());
@@ -890,9 +896,11 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         if (pl.jit) {
             std::string err;
             CUfunction f;
-            int jrc = g_jit.get_nospill(c->device, pl.kb, &f, &err);
-            if (!jrc && !(flags & LMT_MEASURE_SKIP_OPT)) jrc = g_jit.get_nospill(c->device, pl.ko, &f, &err);
+            JitKey gb = pl.kb, go = pl.ko;
+            int jrc = g_jit.get(c->device, pl.kb, &f, &gb, &err);
+            if (!jrc && !(flags & LMT_MEASURE_SKIP_OPT) && pl.feasible) jrc = g_jit.get(c->device, pl.ko, &f, &go, &err);
             if (jrc) { m.status = fail(LMT_ERR_CUDA, "%s", err.c_str()); continue; }
+            m.kernel_id = 10000 + gb.U * 1000 + gb.D * 100 + go.U * 10 + go.D;  // the kernels built
         }
         CUDA_TRY(cudaEventRecord(ev[0], s));
         rc = launch_variant(pl, 0, c->in, rows, cols, pitch, c->in2, c->outb, s);
@@ -994,7 +1002,7 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
     if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
     for (const JitKey &k : keys) {  // load the modules now, not inside a timed batch
         CUfunction f;
-        rc = g_jit.get_nospill(device, k, &f, &err);
+        rc = g_jit.get(device, k, &f, nullptr, &err);
         if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
     }
     if (kernels_out) *kernels_out = (int64_t)keys.size();

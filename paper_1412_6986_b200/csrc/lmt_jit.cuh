@@ -31,6 +31,7 @@
 //   LMT_OPT                              0 baseline (global loads), 1 optimized (TMA -> smem)
 //   LMT_WIDE                             optimized variant with several 256-column TMA chunks
 //   LMT_CTXWRAP                          context counts exceed the in2 halo: reduce indices mod IN2_H/W
+//   LMT_PF                               L1 prefetch distance in steps for the in2 context lines (0 off)
 //   LMT_H2 LMT_W2 LMT_P2                 in2 shape (IN2_H, IN2_W: #defines in the reference too) and
 //                                        its physical pitch, so every context read of a step is
 //                                        one base register plus an immediate offset
@@ -40,8 +41,9 @@ namespace lmt {
 constexpr int SHAPE = LMT_SHAPE, RAD = LMT_R;
 constexpr int CI = LMT_CI, CE = LMT_CE, NC = LMT_NC, NCE = LMT_NCE, NU = LMT_NU, NUE = LMT_NUE;
 constexpr int U = LMT_U, D = LMT_D;
-constexpr int kMaxStagesJ = 8;
+constexpr int kMaxStagesJ = 16;
 constexpr int H2 = LMT_H2, W2 = LMT_W2, P2 = LMT_P2;
+constexpr int PF = LMT_PF;
 
 // ----------------------------------------------------- stencil (kernel_model.py:115-130)
 __host__ __device__ constexpr bool tap_in(int a, int b) {
@@ -110,6 +112,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
         : "memory");
 }
 
+// L1 prefetch: no destination register, so no scoreboard for the step
+// that consumes the line later to wait on.
+__device__ __forceinline__ void prefetch_l1(const float *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 struct alignas(64) TensorMap {
     unsigned long long opaque[16];
 };
@@ -125,17 +133,22 @@ __device__ __forceinline__ void tma_load_2d(float *dst, const TensorMap *map, un
 
 // ----------------------------------------------------- target-array sources
 
-// K1: plain global loads through the read-only path.
+// K1: plain global loads through the read-only path. One uniform base
+// pointer plus a 32-bit element offset per work unit (every `in` index is
+// < 2^31, checked on the host), so a step costs one integer add per work
+// unit instead of a 64-bit pointer update.
 struct GlobalSrc {
-    const float *p[U];  // element (home row, home col) of (i=0, j=0), per work unit
+    const float *base;  // `in` element (PAD, PAD): uniform across the CTA
+    int o[U];           // offset of (home row, home col) of (i=0, j=0), per work unit
     int pitch;
     template <int NU_>
     __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
+        const int step = r * pitch + c;
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
-            const float *q = p[u] + (r * pitch + c);
+            const unsigned q = (unsigned)(o[u] + step);
 #pragma unroll
-            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(q + (tap_dr(k) * pitch + tap_dc(k)));
+            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(base + (q + (unsigned)(tap_dr(k) * pitch + tap_dc(k))));
         }
     }
 };
@@ -215,6 +228,12 @@ __device__ __forceinline__ float ctx_uncoal(const SynthArgs &A, const float *in2
 template <int NU_, class Src>
 __device__ __forceinline__ void fill(Slot<NU_> &s, const Src &src, const Cursor &q, const SynthArgs &A,
                                      const float *in2c, const float *in2u) {
+#if LMT_PF > 0 && !LMT_CTXWRAP
+    // the one new coal row a step touches (rows trow .. trow+NC-1), PF steps
+    // ahead; the uncoal lines only when the walk enters a new 128-byte line
+    if (NC > 0) prefetch_l1(q.crow + (NC - 1 + PF) * P2);
+    if (NU > 0 && ((q.tcol + NU - 1 + PF) & 31) == 0) prefetch_l1(q.ucol + (NU - 1 + PF));
+#endif
     src.template load<NU_>(s.v, q.r, q.c);
 #pragma unroll
     for (int k = 0; k < NC; ++k) s.c[k] = ctx_coal(A, in2c, q.crow, q.trow, k);
@@ -281,7 +300,19 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, co
             fill<NU_>(s[d], src, q, A, in2c, in2u);
             advance(q, A, in2c, in2u);
         }
-    for (int t0 = 0; t0 < NM; t0 += D) {
+    int t0 = 0;
+    // steady state: whole blocks of D steps whose prefetches are all in range,
+    // straight-line (no per-step guards) so each slot's loads can sit on
+    // their own dependency scoreboard
+    for (; t0 + 2 * D - 1 <= NM; t0 += D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            fill<NU_>(s[(d + D - 1) % D], src, q, A, in2c, in2u);
+            advance(q, A, in2c, in2u);
+            consume<NU_>(acc, s[d]);
+        }
+    }
+    for (; t0 < NM; t0 += D) {
 #pragma unroll
         for (int d = 0; d < D; ++d) {
             const int t = t0 + d;
@@ -333,12 +364,13 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const Synth
     for (; it + U <= nit; it += U) {
         GlobalSrc src;
         src.pitch = A.P;
+        src.base = in0;
         size_t o[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int ix = (it + u) % A.nwx, iy = (it + u) / A.nwx;
             const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
-            src.p[u] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
+            src.o[u] = (A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y;
             o[u] = (size_t)wu_y * A.out_w + wu_x;
         }
         float acc[U];
@@ -351,7 +383,8 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const Synth
         const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
         GlobalSrc src;
         src.pitch = A.P;
-        src.p[0] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
+        src.base = in0;
+        src.o[0] = (A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y;
         float acc[1];
         run_units<1>(A, src, in2c, in2u, acc);
         A.out[(size_t)wu_y * A.out_w + wu_x] = acc[0];

@@ -361,7 +361,7 @@ __global__ void k_fill(float *__restrict__ dst, int64_t rows, int64_t cols, int6
 // Fill the wrapped halo of a physical in2 buffer from its interior
 // (rows >= H2 or columns in [W2, P2) get interior cell (r % H2, c % W2)).
 __global__ void k_in2_halo(float *__restrict__ buf, int H2, int W2, int P2) {
-    const int64_t rows = (int64_t)H2 + kIn2HaloRows;
+    const int64_t rows = (int64_t)H2 + kIn2PhysHaloRows;
     const int64_t total = rows * P2;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = v / P2, c = v - r * P2;

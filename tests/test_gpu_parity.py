@@ -13,12 +13,16 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module", autouse=True)
-def _cuda():
+def _cuda(golden):
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     torch.cuda.set_device(0)
+    # compile every specialised kernel the module launches up front, in
+    # parallel host threads (the reference's per-kernel compile step)
+    insts = [make_instance(r) for r in golden["interp"]] + [make_instance(golden["cfg1"])]
+    L.prepare_instances(insts)
 
 
 def test_fill_matches_hash_kat(golden):
@@ -125,6 +129,7 @@ def test_full_size_sweep_instances():
     rng = np.random.default_rng(5)
     rows = rng.choice(len(tab), size=40, replace=False)
     cost = L.sweep.estimated_cost(tab.records(rows))
+    L.prepare_records(tab.records(rows))
     for r, c in zip(rows, cost):
         inst = tab.instance(int(r))
         if c > 0.5 or L.footprint(inst).bytes > 48 * 1024:
