@@ -166,6 +166,17 @@ def cpu_sample(L, table, rows, budget_s: float):
     return rate, cores, desc
 
 
+def fp32_peak_tflops():
+    """fp32 FMA peak: measured by tools/probes/fp32_peak.cu on this pool's
+    B200 (profiles/fp32_peak.json), else the nominal 148 SMs x 128 lanes x 2
+    flops x 1.965 GHz."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp32_peak.json")))
+        return float(d["fp32_fma_tflops"]), "measured (profiles/fp32_peak.json)"
+    except (OSError, ValueError, KeyError):
+        return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal (148 SMs x 128 lanes x 2 x 1.965 GHz)"
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -279,7 +290,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     except (OSError, ValueError):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+    hbm_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    fp32_peak, fp32_src = fp32_peak_tflops()
+    roof = L.measure.roofline(res_all, hbm_peak, fp32_peak)
+    floor = L.measure.launch_floor(table.records(rows_all), res_all, hbm_peak)
     gpu_launches = int(res_all["launches"].sum())
     if args.dump:
         np.savez(args.dump if world == 1 else f"{args.dump}.rank{rank}", rows=rows_all,
@@ -310,12 +324,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "instances_timed": n_total, "labels_gathered": n_labels, "verified_bitwise": verified,
         "mismatched": mismatched, "failed": failed,
         "kernel_ms": k_ms, "fill_ms": fill_ms, "step_ms_total": max_ms,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
-                     "kernel": "k_synth_base + k_synth_opt (all launches of the timed steps)",
-                     "note": "algorithmic bytes 4*(|U_in|+|U_in2|+out) per variant (SURVEY 8(d)) over summed "
-                             "CUDA-event kernel time; most sweep instances are fp32/LSU-issue bound"},
-        "fp32": {"achieved_tflops": k_flops / (k_ms / 1e3) / 1e12 if k_ms else 0.0},
+        "roofline": dict(roof, traffic=None, peak_source={"hbm": hbm_src, "fp32": fp32_src},
+                         kernel="lmt_kernel (K1 baseline + K2 optimized, NVRTC-specialised), all launches of the "
+                                "timed steps",
+                         note="per launch: algorithmic bytes 4*(|U_in|+|U_in2|+out) at the HBM peak vs algorithmic "
+                              "flops (MAD=2) at the fp32 peak, SURVEY 8(d); achieved/frac on the dominant roof, "
+                              "frac_of_binding = sum of per-launch roof times / sum of measured times"),
+        "launch_floor": dict(floor, note="per launch max(HBM bytes/peak, per-thread chain floor, per-SM issue "
+                                         "floor) with the workgroup->CTA mapping fixed (sweep.floor_seconds); frac "
+                                         "= sum of floors / sum of measured kernel times"),
         "gpu_launches": gpu_launches,
         "jit": {"kernels": n_kernels, "compiled": jit_compiled, "compile_s": round(jit_seconds, 2),
                 "prepare_wall_s": round(t_prep, 2),

@@ -192,9 +192,69 @@ def measure_instances_host(instances, in_arrays, in2_arrays, dev=DEFAULT_DEVICE,
     return _convert(instances, out[:n])
 
 
+def launch_floor(records: np.ndarray, res: np.ndarray, hbm_gbs: float) -> dict:
+    """How close the measured launches are to what their own launch shape
+    allows: per launch max(HBM bytes / peak, chain floor, per-SM issue floor)
+    (sweep.floor_seconds), summed over both variants, over summed measured
+    time."""
+    from .sweep import floor_seconds
+
+    ch, iss = floor_seconds(records)
+    fl, t = [], []
+    for col in ("t_base_ms", "t_opt_ms"):
+        ran = res[col] > 0
+        fl.append(np.maximum(np.maximum(ch[ran], iss[ran]), res["alg_bytes"][ran] / (hbm_gbs * 1e9)))
+        t.append(res[col][ran] / 1e3)
+    fl, t = np.concatenate(fl), np.concatenate(t)
+    return {"frac": float(fl.sum() / t.sum()) if t.sum() > 0 else 0.0, "floor_s": float(fl.sum()),
+            "kernel_s": float(t.sum())}
+
+
+def roofline(res: np.ndarray, hbm_gbs: float, fp32_tflops: float) -> dict:
+    """Roofline accounting of measured launches (a MEASUREMENT_DTYPE array,
+    both variants): each launch is bound by the slower of its
+    algorithmic HBM bytes at ``hbm_gbs`` and its algorithmic fp32 flops (MAD =
+    2) at ``fp32_tflops``.
+
+    Returns the dominant roof over the set (the one that carries more of the
+    summed roof time), achieved = algorithmic bytes (or flops) / summed
+    kernel time against that peak, and ``frac_of_binding`` = summed per-launch
+    roof time / summed measured time, i.e. how close the launches are to
+    their own binding roofs."""
+    t, b, f = [], [], []
+    for col in ("t_base_ms", "t_opt_ms"):
+        ran = res[col] > 0
+        t.append(res[col][ran] / 1e3)
+        b.append(res["alg_bytes"][ran])
+        f.append(res["alg_flops"][ran])
+    t, b, f = np.concatenate(t), np.concatenate(b), np.concatenate(f)
+    if t.size == 0 or t.sum() <= 0:
+        return {}
+    t_hbm = b / (hbm_gbs * 1e9)
+    t_fp = f / (fp32_tflops * 1e12)
+    roof = np.maximum(t_hbm, t_fp)
+    hbm_bound = t_hbm >= t_fp
+    dominant = "hbm" if roof[hbm_bound].sum() >= roof[~hbm_bound].sum() else "fp32"
+    T = float(t.sum())
+    out = {"bound": dominant, "launches": int(t.size), "kernel_s": T,
+           "frac_of_binding": float(roof.sum() / T),
+           "hbm_bound_launches": int(hbm_bound.sum()), "fp32_bound_launches": int((~hbm_bound).sum())}
+    if dominant == "hbm":
+        ach = float(b.sum() / T / 1e9)
+        out.update(achieved=ach, peak=hbm_gbs, unit="GB/s", frac=ach / hbm_gbs)
+    else:
+        ach = float(f.sum() / T / 1e12)
+        out.update(achieved=ach, peak=fp32_tflops, unit="TFLOP/s", frac=ach / fp32_tflops)
+    if hbm_bound.any():  # the memory-bound subset on its own roof
+        tb = float(t[hbm_bound].sum())
+        out["hbm_subset"] = {"achieved": float(b[hbm_bound].sum() / tb / 1e9), "peak": hbm_gbs, "unit": "GB/s",
+                             "frac": float(b[hbm_bound].sum() / tb / 1e9 / hbm_gbs), "kernel_s": tb}
+    return out
+
+
 def error_of(m: Measurement) -> str:
     return STATUS_NAMES.get(m.status, f"status {m.status}")
 
 
-__all__ = ["Measurement", "measure_instances", "measure_instances_host", "measure_raw", "prepare_records",
+__all__ = ["Measurement", "roofline", "measure_instances", "measure_instances_host", "measure_raw", "prepare_records",
            "prepare_instances", "last_error"]

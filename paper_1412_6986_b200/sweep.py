@@ -270,27 +270,30 @@ def chain_ops(records: np.ndarray) -> np.ndarray:
     return rec[:, 5] * rec[:, 6] * (K + rec[:, 9] + rec[:, 11] + rec[:, 13]) + rec[:, 10] + rec[:, 12] + rec[:, 14]
 
 
-def floor_seconds(records: np.ndarray, clock_hz: float = 1.965e9, sms: int = 148,
-                  lanes_per_sm: int = 128) -> tuple[np.ndarray, np.ndarray]:
-    """Per-variant lower bounds on one launch of each instance, with the
-    workgroup -> CTA, workitem -> thread mapping fixed:
+def floor_seconds(records: np.ndarray, clock_hz: float = 1.965e9, sms: int = 148) -> tuple[np.ndarray, np.ndarray]:
+    """Per-variant lower bounds on one launch of each instance with the
+    reference's mapping fixed (workgroup -> CTA on one SM, workitem -> thread):
 
     - chain: a workitem's work units are independent but each is a serial
-      chain of fp32 ops (bit-exact order), so a thread needs at least
-      wus * chain issue cycles even with full ILP across its work units;
-    - issue: every warp slot (partial warps included) issues each op once,
-      over 148 SMs x 128 fp32 lanes.
+      chain of fp32 ops in a fixed order (bit-exact), and a warp issues at
+      most one instruction per cycle, so a thread needs >= wus * chain cycles
+      however its work units are interleaved;
+    - issue: a CTA's warps share one SM's four schedulers, and the CTAs are
+      spread over at most 148 SMs: ceil(ctas / 148) * warps_per_cta * wus *
+      chain / 4 cycles (partial warps pay for 32 lanes).
 
-    Returns (chain_floor_s, issue_floor_s)."""
+    Returns (chain_floor_s, issue_floor_s); the HBM floor is alg_bytes /
+    peak (see measure.roofline)."""
     rec = np.asarray(records, dtype=np.int64)
-    chain = chain_ops(rec)
+    chain = chain_ops(rec).astype(np.float64)
     grid = rec[:, 15] * rec[:, 16]
-    wg = rec[:, 17] * rec[:, 18]
+    wg = np.maximum(rec[:, 17] * rec[:, 18], 1)
     wus = rec[:, 2] * rec[:, 3] // np.maximum(grid, 1)
-    warps = (grid // np.maximum(wg, 1)) * ((wg + 31) // 32)
+    ctas = grid // wg
+    warps = (wg + 31) // 32
     chain_s = wus * chain / clock_hz
-    issue_s = warps * 32.0 * wus * chain / (sms * lanes_per_sm * clock_hz)
-    return chain_s.astype(np.float64), issue_s
+    issue_s = np.ceil(ctas / sms) * warps * wus * chain / 4.0 / clock_hz
+    return chain_s, issue_s
 
 
 def shard_balanced(costs: np.ndarray, world: int) -> list[np.ndarray]:
