@@ -68,10 +68,7 @@ def step_rows(perm, step: int, world: int, batch: int):
 
 
 def shard_for_rank(L, table, rows, world: int, rank: int):
-    if world == 1:
-        return rows
-    cost = L.sweep.estimated_cost(table.records(rows))
-    return rows[L.sweep.shard_balanced(cost, world)[rank]]
+    return L.dist.rank_rows(table, rows, world, rank)
 
 
 # ------------------------------------------------------------------ clocks
@@ -258,19 +255,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- labels: NCCL all-gather of (row, t_base, t_opt) -- the only collective
     rows_all = np.concatenate([r for r, _ in results])
     res_all = np.concatenate([x for _, x in results])
-    lab = torch.tensor(np.stack([rows_all.astype(np.float64), res_all["t_base_ms"], res_all["t_opt_ms"]], 1),
-                       device="cuda", dtype=torch.float64)
-    if world > 1:
-        sizes = [torch.zeros(1, device="cuda", dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(sizes, torch.tensor([lab.shape[0]], device="cuda", dtype=torch.int64))
-        mx = int(max(s.item() for s in sizes))
-        pad = torch.zeros((mx, 3), device="cuda", dtype=torch.float64)
-        pad[: lab.shape[0]] = lab
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad)
-        labels = torch.cat([b[: int(s.item())] for b, s in zip(bufs, sizes)])
-    else:
-        labels = lab
+    labels = L.dist.all_gather_labels(L.dist.label_matrix(rows_all, res_all), device="cuda")
     n_labels = int(labels.shape[0])
 
     # ---- per-kernel accounting (the synthetic kernels are the dominant launches)

@@ -169,6 +169,21 @@ void lmt_rf_destroy(lmt_forest *f);
 int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
                 int32_t nthreads, int64_t *kernels_out);
 
+/* K4: the feature vector and modelled label of n instances on the GPU
+ * (access_analysis.extract_features, access_analysis.py:272-308, and
+ * cost_model.label_speedup with the coalescing override build_dataset passes,
+ * cost_model.py:94-158, dataset.py:264-271), bit-identical to the reference.
+ * devs: ndev == 1 descriptor for all instances or ndev == n (NULL: defaults).
+ * coal_override[i] (NaN = none) / lmem_override[i] (< 0 = none) may be NULL.
+ * Outputs (host): X [n][18] in FEATURE_NAMES order, label [n] (0.0 when the
+ * optimized variant is infeasible), times [n][8] = kernel_time of the
+ * baseline then the optimized variant (compute_cycles, mem_transactions,
+ * active_warps, total_cycles; NaN when infeasible; may be NULL), status [n]:
+ * 0 ok, 1 invalid instance (X, label NaN), 2 infeasible, 5 unsupported device. */
+int lmt_features(const lmt_instance *insts, int64_t n, const lmt_device *devs, int64_t ndev,
+                 const double *coal_override, const int64_t *lmem_override, double *h_X,
+                 double *h_label, double *h_times, int32_t *h_status);
+
 /* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
  * compiles) and the host seconds spent compiling. */
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);

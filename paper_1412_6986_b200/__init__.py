@@ -9,6 +9,16 @@ liblmt_b200.so (hand-written sm_100a CUDA behind a C ABI, include/lmt_b200.h);
 there is no CPU fallback.
 """
 
+from . import access_analysis, dist, measure, sweep  # noqa: F401
+from .access_analysis import (
+    FEATURE_NAMES,
+    FeatureVector,
+    TimeEstimate,
+    extract_features,
+    features_records,
+    kernel_time,
+    label_speedup,
+)
 from .device import DEFAULT_DEVICE, DeviceDescriptor
 from .errors import (
     ConfigError,

@@ -78,7 +78,7 @@ EXPORTS = (
     "lmt_version", "lmt_last_error", "lmt_validate", "lmt_emit_geometry", "lmt_fill",
     "lmt_execute", "lmt_measure_batch", "lmt_measure_batch_host", "lmt_digest",
     "lmt_rf_create", "lmt_rf_mean", "lmt_rf_mean_host", "lmt_rf_destroy", "lmt_sync",
-    "lmt_get_stream", "lmt_prepare", "lmt_jit_stats",
+    "lmt_get_stream", "lmt_prepare", "lmt_jit_stats", "lmt_features",
 )
 
 _lib = None
@@ -111,6 +111,7 @@ def _declare(L):
     L.lmt_get_stream.argtypes = [P(vp)]
     L.lmt_prepare.argtypes = [P(CInstance), c_i64, P(CDevice), c_i32, c_i32, P(c_i64)]
     L.lmt_jit_stats.argtypes = [P(c_i64), P(ctypes.c_double)]
+    L.lmt_features.argtypes = [P(CInstance), c_i64, P(CDevice), c_i64, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("lmt_version", "lmt_last_error", "lmt_rf_destroy"):

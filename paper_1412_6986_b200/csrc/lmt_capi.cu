@@ -19,6 +19,7 @@
 #include "lmt_kernels.cuh"
 #include "lmt_synth_ilp.cuh"
 #include "lmt_jit_host.cuh"
+#include "lmt_features.cuh"
 
 #ifndef LMT_VERSION
 #define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
@@ -1006,6 +1007,67 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
         if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
     }
     if (kernels_out) *kernels_out = (int64_t)keys.size();
+    return LMT_OK;
+}
+
+int lmt_features(const lmt_instance *insts, int64_t n, const lmt_device *devs, int64_t ndev,
+                 const double *coal_override, const int64_t *lmem_override, double *h_X, double *h_label,
+                 double *h_times, int32_t *h_status) {
+    if (n < 0 || (n > 0 && (!insts || !h_X || !h_label || !h_status)) || (ndev != 1 && ndev != n && devs))
+        return fail(LMT_ERR_ARG, "bad features arguments");
+    if (n == 0) return LMT_OK;
+    static_assert(sizeof(lmt_instance) == sizeof(FeatInst), "lmt_instance layout");
+    static_assert(sizeof(lmt_device) == sizeof(FeatDev), "lmt_device layout");
+    DevCtx *c;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int rc = get_ctx(&c);
+        if (rc) return rc;
+    }
+    const lmt_device dflt = kDefaultDevice;
+    if (!devs) { devs = &dflt; ndev = 1; }
+    int max_tx = 0, max_w = 0;
+    for (int64_t k = 0; k < ndev; k++) {
+        max_tx = std::max(max_tx, std::min(devs[k].transaction_bytes, kFeatMaxTx));
+        max_w = std::max(max_w, devs[k].warp_size);
+    }
+    const int smem_longs = 3 * std::max(max_tx, 1) + (max_w > 32 ? std::min(max_w, 1024) : 0);
+    const size_t smem = (size_t)smem_longs * 8 * 4;  // 4 warps per CTA
+    if (smem > c->smem_optin - 1024) return fail(LMT_ERR_ARG, "device descriptor too large for K4");
+    cudaStream_t s = c->stream;
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_features),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    char *buf = nullptr;
+    const size_t bi = (size_t)n * sizeof(lmt_instance), bd = (size_t)ndev * sizeof(lmt_device);
+    const size_t bco = coal_override ? (size_t)n * 8 : 0, blo = lmem_override ? (size_t)n * 8 : 0;
+    const size_t bx = (size_t)n * 18 * 8, bl = (size_t)n * 8, bt = h_times ? (size_t)n * 64 : 0, bs = (size_t)n * 4;
+    auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+    const size_t total = al(bi) + al(bd) + al(bco) + al(blo) + al(bx) + al(bl) + al(bt) + al(bs);
+    CUDA_TRY(cudaMallocAsync(&buf, total, s));
+    char *q = buf;
+    auto take = [&](size_t b) { char *r = q; q += al(b); return r; };
+    FeatInst *d_i = (FeatInst *)take(bi);
+    FeatDev *d_d = (FeatDev *)take(bd);
+    double *d_co = bco ? (double *)take(bco) : nullptr;
+    long long *d_lo = blo ? (long long *)take(blo) : nullptr;
+    double *d_x = (double *)take(bx), *d_l = (double *)take(bl);
+    double *d_t = bt ? (double *)take(bt) : nullptr;
+    int *d_s = (int *)take(bs);
+    CUDA_TRY(cudaMemcpyAsync(d_i, insts, bi, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(d_d, devs, bd, cudaMemcpyHostToDevice, s));
+    if (d_co) CUDA_TRY(cudaMemcpyAsync(d_co, coal_override, bco, cudaMemcpyHostToDevice, s));
+    if (d_lo) CUDA_TRY(cudaMemcpyAsync(d_lo, lmem_override, blo, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(d_s, 0xff, bs, s));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 3) / 4, (int64_t)c->sms * 16));
+    k_features<<<(unsigned)blocks, 128, smem, s>>>(d_i, n, d_d, (int)ndev, d_co, d_lo, d_x, d_l, d_t, d_s,
+                                                   smem_longs);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(h_X, d_x, bx, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(h_label, d_l, bl, cudaMemcpyDeviceToHost, s));
+    if (d_t) CUDA_TRY(cudaMemcpyAsync(h_times, d_t, bt, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(h_status, d_s, bs, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaFreeAsync(buf, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return LMT_OK;
 }
 

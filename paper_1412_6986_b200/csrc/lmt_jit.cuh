@@ -134,9 +134,8 @@ __device__ __forceinline__ void tma_load_2d(float *dst, const TensorMap *map, un
 // ----------------------------------------------------- target-array sources
 
 // K1: plain global loads through the read-only path. One uniform base
-// pointer plus a 32-bit element offset per work unit (every `in` index is
-// < 2^31, checked on the host), so a step costs one integer add per work
-// unit instead of a 64-bit pointer update.
+// pointer plus a signed 32-bit element offset per work unit (every `in`
+// index is < 2^31, checked on the host).
 struct GlobalSrc {
     const float *base;  // `in` element (PAD, PAD): uniform across the CTA
     int o[U];           // offset of (home row, home col) of (i=0, j=0), per work unit
@@ -146,9 +145,9 @@ struct GlobalSrc {
         const int step = r * pitch + c;
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
-            const unsigned q = (unsigned)(o[u] + step);
+            const int q = o[u] + step;  // signed: taps above/left of the home element are negative
 #pragma unroll
-            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(base + (q + (unsigned)(tap_dr(k) * pitch + tap_dc(k))));
+            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(base + (q + (tap_dr(k) * pitch + tap_dc(k))));
         }
     }
 };

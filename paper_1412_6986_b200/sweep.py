@@ -318,6 +318,18 @@ def shard_contiguous(costs: np.ndarray, world: int) -> list[np.ndarray]:
     return [np.arange(cuts[w], cuts[w + 1]) for w in range(world)]
 
 
+def instances_to_records(instances) -> np.ndarray:
+    """int32 [n, 19] records of KernelInstance-shaped objects (ours or the reference's)."""
+    rows = []
+    for inst in instances:
+        p, lc = inst.params, inst.launch
+        rows.append((p.in_h, p.in_w, p.out_h, p.out_w, PATTERN_ORDER.index(getattr(p.pattern, "value", p.pattern)),
+                     p.n, p.m, SHAPE_ORDER.index(getattr(p.stencil.shape, "value", p.stencil.shape)),
+                     p.stencil.radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb, p.num_coal_ep,
+                     p.num_uncoal_ilb, p.num_uncoal_ep, lc.grid_x, lc.grid_y, lc.wg_x, lc.wg_y))
+    return np.array(rows, dtype=np.int32).reshape(-1, 19)
+
+
 def records_to_c(records: np.ndarray):
     from ._lib import CInstance
 

@@ -119,6 +119,46 @@ def interp_cases():
     return cases
 
 
+def _rec19(inst):
+    p, lc = inst.params, inst.launch
+    return [p.in_h, p.in_w, p.out_h, p.out_w, list(HomeAccessPattern).index(p.pattern), p.n, p.m,
+            list(StencilShape).index(p.stencil.shape), p.stencil.radius, p.num_comp_ilb, p.num_comp_ep,
+            p.num_coal_ilb, p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, lc.grid_x, lc.grid_y, lc.wg_x, lc.wg_y]
+
+
+def feature_fixture():
+    """features.npz: rec [n,19] int32, X [n,18] f64, label [n] f64 (label_speedup with the coalescing
+    override, exactly build_dataset's label, dataset.py:264-271), dev [n,10] int32 device descriptor."""
+    from lmtune.device import DeviceDescriptor
+
+    insts = dataset._select_instances(dataset.SamplingSpec(max_instances=20000, seed=5))
+    rng = np.random.default_rng(11)
+    devs = [DeviceDescriptor()] * len(insts)
+    # non-default devices: other warp / transaction sizes, capacities, latencies
+    alt = [DeviceDescriptor(transaction_bytes=64, warp_size=16, lmem_capacity_bytes=16 * 1024),
+           DeviceDescriptor(transaction_bytes=256, warp_size=64, max_regs_per_thread=255,
+                            register_file_per_sm=65536, max_warps_per_sm=64, max_workgroups_per_sm=32,
+                            dram_latency_cycles=600, issue_cycles_per_op=2, lmem_capacity_bytes=227 * 1024),
+           DeviceDescriptor(transaction_bytes=32, warp_size=32, element_bytes=4)]
+    extra = [insts[i] for i in rng.choice(len(insts), size=600, replace=False)]
+    insts = insts + extra * len(alt)
+    devs = devs + [d for d in alt for _ in extra]
+    rec, X, lab, dv = [], [], [], []
+    for inst, d in zip(insts, devs):
+        fv = aa.extract_features(inst, d)
+        rec.append(_rec19(inst))
+        X.append(fv.to_array())
+        lab.append(cost_model.label_speedup(inst, d, coalescing_override=fv.noncoalescing_degree))
+        dv.append([getattr(d, f) for f in ("transaction_bytes", "warp_size", "element_bytes",
+                                            "lmem_capacity_bytes", "register_file_per_sm", "max_regs_per_thread",
+                                            "max_warps_per_sm", "max_workgroups_per_sm", "dram_latency_cycles",
+                                            "issue_cycles_per_op")])
+    np.savez_compressed(os.path.join(OUT, "features.npz"), rec=np.array(rec, dtype=np.int32),
+                        X=np.array(X, dtype=np.float64), label=np.array(lab, dtype=np.float64),
+                        dev=np.array(dv, dtype=np.int32))
+    print("features:", len(rec), "rows")
+
+
 def main():
     golden = {}
     # 1. hash KAT (interp.py:22-27)
@@ -194,6 +234,9 @@ def main():
     golden["forest"] = dict(rows=len(X), trees=len(f.trees), nodes=int(sum(len(t.feature) for t in f.trees)))
     # 7. cost-model label KAT + features for the same held-out rows (K4 next)
     golden["labels"] = [float(cost_model.label_speedup(r.instance)) for r in ev[:200]]
+    # 8. features + modelled labels (K4, access_analysis.py:272-308, cost_model.py:94-158) for every
+    #    instance of a 20k-instance selection plus non-default devices
+    feature_fixture()
     with open(os.path.join(OUT, "golden.json"), "w") as fh:
         json.dump(golden, fh, indent=0, sort_keys=True)
     print("wrote", len(recs), "interp cases,", len(geo), "geometry rows")

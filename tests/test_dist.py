@@ -1,0 +1,70 @@
+"""The N>1 host path on CPU: world-size-2 gloo processes shard a sweep batch
+disjointly by cost and all-gather the label blocks (the only collective;
+NCCL on the GPU box)."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import paper_1412_6986_b200 as L
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        table = L.select_instance_table(L.SamplingSpec(max_instances=5000, seed=3))
+        rows = np.random.default_rng(7).permutation(len(table))[:97]
+        mine = L.dist.rank_rows(table, rows, world, rank)
+        # stand-in measurements (the GPU fills these): deterministic per row
+        res = np.zeros(len(mine), dtype=L.measure.MEASUREMENT_DTYPE)
+        res["t_base_ms"] = mine * 0.5 + 1.0
+        res["t_opt_ms"] = np.where(mine % 3 == 0, -1.0, mine * 0.25 + 2.0)
+        labels = L.dist.all_gather_labels(L.dist.label_matrix(mine, res))
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), mine=mine, labels=labels, rows=rows)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_shard_and_label_gather(tmp_path):
+    torch = pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    rows = got[0]["rows"]
+    mine = [g["mine"] for g in got]
+    # disjoint and complete
+    assert len(np.intersect1d(mine[0], mine[1])) == 0
+    assert np.array_equal(np.sort(np.concatenate(mine)), np.sort(rows))
+    # every rank holds every label, sorted by row, values intact
+    for g in got:
+        lab = g["labels"]
+        assert np.array_equal(lab[:, 0], np.sort(rows).astype(np.float64))
+        r = lab[:, 0]
+        assert np.array_equal(lab[:, 1], r * 0.5 + 1.0)
+        assert np.array_equal(lab[:, 2], np.where(r % 3 == 0, -1.0, r * 0.25 + 2.0))
+    assert np.array_equal(got[0]["labels"], got[1]["labels"])
+    # cost balance: neither shard carries much more than half of the estimate
+    import paper_1412_6986_b200 as L
+
+    table = L.select_instance_table(L.SamplingSpec(max_instances=5000, seed=3))
+    cost = [L.sweep.estimated_cost(table.records(m)).sum() for m in mine]
+    assert max(cost) / sum(cost) < 0.6
+    del torch

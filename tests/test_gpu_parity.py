@@ -172,3 +172,37 @@ def test_reference_objects_accepted(lmtune_ref):
     b, o = L.run_pair(k)
     rb, ro = ref_run_pair(k)
     assert np.array_equal(b, rb) and np.array_equal(o, ro)
+
+
+def _golden_devices(dv):
+    return [L.DeviceDescriptor(*[int(x) for x in row]) for row in dv]
+
+
+def test_features_and_labels_bitwise():
+    """K4 against the reference's extract_features + label_speedup on 21.8k
+    rows (20k sweep instances at the default device, 600 x 3 other devices)."""
+    g = np.load(f"{GOLDEN_DIR}/features.npz")
+    rec, X, lab, dv = g["rec"], g["X"], g["label"], g["dev"]
+    default = (dv == dv[0]).all(axis=1)
+    b = L.features_records(rec[default], L.DEFAULT_DEVICE)
+    assert (b.status[default[default]] != 1).all()
+    assert np.array_equal(b.X, X[default])
+    assert np.array_equal(b.label, lab[default])
+    other = ~default
+    b2 = L.features_records(rec[other], _golden_devices(dv[other]))
+    assert np.array_equal(b2.X, X[other])
+    assert np.array_equal(b2.label, lab[other])
+
+
+def test_feature_api_single_instance(golden):
+    r = golden["interp"][3]
+    inst = make_instance(r)
+    fv = L.extract_features(inst)
+    b = L.features_instances([inst]) if hasattr(L, "features_instances") else L.access_analysis.features_instances([inst])
+    assert np.array_equal(fv.to_array(), b.X[0])
+    assert L.label_speedup(inst) == b.label[0]
+    tb = L.kernel_time(inst, L.Variant.BASELINE)
+    assert tb.total_cycles == b.times[0, 3]
+    bad = L.KernelInstance(inst.params, L.LaunchConfig(16, 16, 8, 8))
+    with pytest.raises(L.InvalidInstance):
+        L.extract_features(bad)
