@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-rf", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dump", default=None, help="save per-instance records and measurements (npz)")
     return ap.parse_args()
@@ -288,6 +289,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, L, table, perm, world, rank, barrier)
+    rf = None if args.no_rf else run_rf(args, L, world, rank, barrier)
 
     if rank != 0:
         return
@@ -326,9 +328,85 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     }
     if e2e:
         line["e2e"] = e2e
+    if rf:
+        line["rf"] = rf
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def run_rf(args, L, world, rank, barrier):
+    """BASELINE config 4 beside the sweep: the reference model trained on 10%
+    of a 100k sweep (tests/golden/forest_sweep100k.txt.gz, made by the
+    reference), the held-out 90% featurised on the GPU (K4) and predicted (K3);
+    predictions checked bitwise against the reference's. Rows shard
+    contiguously across ranks; times are max over ranks."""
+    import gzip
+    import hashlib
+    import tempfile
+
+    import torch
+    import torch.distributed as dist
+
+    gdir = os.path.join(ROOT, "tests", "golden")
+    ev = np.load(os.path.join(gdir, "forest_sweep100k_eval.npz"))
+    with gzip.open(os.path.join(gdir, "forest_sweep100k.txt.gz"), "rb") as fh, \
+            tempfile.NamedTemporaryFile(suffix=".txt", delete=False) as out:
+        out.write(fh.read())
+    forest = L.load(out.name)
+    os.unlink(out.name)
+    table = L.select_instance_table(L.SamplingSpec(max_instances=100_000, seed=0))
+    held = ev["held_idx"]
+    mine = np.array_split(held, world)[rank]
+    rec = table.records(mine)
+    L.features_records(rec[:64])  # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    fb = L.features_records(rec)
+    t_feat = time.perf_counter() - t0
+    g = L.forest.gpu_forest(forest)
+    X_t = torch.tensor(fb.X, device="cuda")
+    out_t = torch.empty(len(mine), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        g.mean_device(X_t, out_t, stream=stream.cuda_stream)
+    reps = max(3, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for _ in range(reps):
+        g.mean_device(X_t, out_t, stream=stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_k3 = e0.elapsed_time(e1) / 1e3 / reps
+    t0 = time.perf_counter()
+    pred = L.predict(forest, fb.X)  # host X in, host predictions out (2 ** mean in numpy)
+    t_e2e = time.perf_counter() - t0
+    t = torch.tensor([t_feat, t_k3, t_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_feat, t_k3, t_e2e = (float(v) for v in t.tolist())
+    out = {"workload": "config 4: reference forest (20 trees, 4 features/node, trained on 10% of "
+                       "SamplingSpec(100k, seed=0)), held-out 90% = 90,000 rows",
+           "trees": len(forest.trees), "nodes": int(sum(len(tr.feature) for tr in forest.trees)),
+           "rows": int(len(held)), "k3_rows_per_s": len(held) / t_k3,
+           "predict_e2e_rows_per_s": len(held) / t_e2e, "k4_features_rows_per_s": len(held) / t_feat}
+    if world == 1:
+        out["features_bitwise_reference"] = hashlib.sha256(fb.X.tobytes()).digest() == ev["X_sha256"].tobytes()
+        out["predictions_bitwise_reference"] = bool(
+            hashlib.sha256(pred.tobytes()).digest() == ev["pred_sha256"].tobytes()
+            and np.array_equal(pred[::8], ev["pred_every8"]))
+        if not args.no_cpu and rank == 0:
+            import oracle
+
+            n = min(len(held), 20000)
+            t0 = time.perf_counter()
+            oracle.forest_mean(forest.trees, fb.X[:n], nthreads=1)
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": n / dt, "unit": "rows/s", "cores": 1, "kind": "port",
+                                   "sample": f"oracle C port of forest.predict's tree walk on {n} held-out rows"}
+    return out
 
 
 def run_e2e(args, L, table, perm, world, rank, barrier):
@@ -337,7 +415,7 @@ def run_e2e(args, L, table, perm, world, rank, barrier):
     host memory inside the timed region."""
     import torch
 
-    steps = range(args.warmup, args.warmup + max(1, min(args.steps, 2)))
+    steps = range(args.warmup, args.warmup + args.steps)  # the same steps as the device-timed region
     plan = []
     host_in = {}
     in2_host = None

@@ -9,7 +9,7 @@ liblmt_b200.so (hand-written sm_100a CUDA behind a C ABI, include/lmt_b200.h);
 there is no CPU fallback.
 """
 
-from . import access_analysis, dist, measure, sweep  # noqa: F401
+from . import access_analysis, dataset, dist, measure, sweep  # noqa: F401
 from .access_analysis import (
     FEATURE_NAMES,
     FeatureVector,
@@ -19,6 +19,7 @@ from .access_analysis import (
     kernel_time,
     label_speedup,
 )
+from .dataset import BuildResult, LabeledInstance, build_arrays, build_dataset, split_rows
 from .device import DEFAULT_DEVICE, DeviceDescriptor
 from .errors import (
     ConfigError,

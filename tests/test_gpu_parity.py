@@ -206,3 +206,26 @@ def test_feature_api_single_instance(golden):
     bad = L.KernelInstance(inst.params, L.LaunchConfig(16, 16, 8, 8))
     with pytest.raises(L.InvalidInstance):
         L.extract_features(bad)
+
+
+def test_config4_forest_on_gpu_features_matches_reference():
+    """BASELINE config 4: the reference model trained on 10% of a 100k sweep;
+    features of the held-out 90% rebuilt on the GPU (K4) and predictions (K3)
+    must be bit-identical to the reference's forest.predict."""
+    import gzip
+    import hashlib
+    import tempfile
+
+    ev = np.load(f"{GOLDEN_DIR}/forest_sweep100k_eval.npz")
+    with gzip.open(f"{GOLDEN_DIR}/forest_sweep100k.txt.gz", "rb") as fh, \
+            tempfile.NamedTemporaryFile(suffix=".txt", delete=False) as out:
+        out.write(fh.read())
+    f = L.load(out.name)
+    table = L.select_instance_table(L.SamplingSpec(max_instances=100_000, seed=0))
+    held = ev["held_idx"]
+    fb = L.features_records(table.records(held))
+    assert hashlib.sha256(fb.X.tobytes()).digest() == ev["X_sha256"].tobytes()
+    pred = L.predict(f, fb.X)
+    assert np.array_equal(pred[::8], ev["pred_every8"])
+    assert hashlib.sha256(pred.tobytes()).digest() == ev["pred_sha256"].tobytes()
+    assert np.array_equal(fb.label[::8], ev["speedup_every8"])

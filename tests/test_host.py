@@ -152,3 +152,28 @@ def test_speedup_to_target():
     assert L.speedup_to_target(1.0) == 0.0
     assert L.speedup_to_target(8.0) == 3.0
     assert L.speedup_to_target(0.0) == -10.0
+
+
+def test_split_matches_reference_fixture():
+    """cli.split_rows (cli.py:54-64) on the 100k selection: the reference's
+    held-out indices of the config-4 fixture."""
+    import numpy as np
+
+    import paper_1412_6986_b200 as L
+    from conftest import GOLDEN_DIR
+
+    ev = np.load(f"{GOLDEN_DIR}/forest_sweep100k_eval.npz")
+    tr, he = L.dataset.split_indices(100_000, 0.10, 0)
+    assert np.array_equal(tr, ev["train_idx"]) and np.array_equal(he, ev["held_idx"])
+    a, b = L.split_rows(list(range(10)), 0.3, 5)
+    assert len(a) == 3 and len(b) == 7 and sorted(a + b) == list(range(10))
+
+
+def test_split_against_reference(lmtune_ref):
+    from lmtune.cli import split_rows as ref_split
+
+    import paper_1412_6986_b200 as L
+
+    rows = list(range(1234))
+    for seed in (0, 1, 99):
+        assert L.split_rows(rows, 0.1, seed) == ref_split(rows, 0.1, seed)
