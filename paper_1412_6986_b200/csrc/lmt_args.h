@@ -43,5 +43,10 @@ constexpr int kIn2HaloCols = 8;
 constexpr int kPfMax = 32;
 constexpr int kIn2PhysHaloRows = kIn2HaloRows + kPfMax;
 constexpr int kIn2PhysHaloCols = kIn2HaloCols + kPfMax;
+// kIn2Copies copies of the (haloed) in2 buffer, copy s shifted left by s
+// columns: copy_s[r][x] = in2[r % IN2_H][(x + s) % IN2_W]. The uncoalesced
+// context reads of a step, in2[glin % IN2_H][t .. t + 3], are then one
+// 16-byte-aligned 128-bit load from copy (t & 3) at column t - (t & 3).
+constexpr int kIn2Copies = 4;
 
 }  // namespace lmt

@@ -322,7 +322,8 @@ struct Plan {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 int64_t in2_pitch(int64_t w) { return round_up(w + kIn2PhysHaloCols, 32); }  // rows start on 128-byte lines
-size_t in2_phys_elems(int64_t h, int64_t w) { return (size_t)(h + kIn2PhysHaloRows) * (size_t)in2_pitch(w); }
+size_t in2_copy_elems(int64_t h, int64_t w) { return (size_t)(h + kIn2PhysHaloRows) * (size_t)in2_pitch(w); }
+size_t in2_phys_elems(int64_t h, int64_t w) { return kIn2Copies * in2_copy_elems(h, w); }
 
 // |U_in2|: union of the in2 cells the context reads touch.
 double in2_union(const lmt_instance &p) {
@@ -678,6 +679,9 @@ int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int sms) {
     const int64_t total = (h + kIn2PhysHaloRows) * in2_pitch(w);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8));
     k_in2_halo<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w));
+    CUDA_TRY(cudaGetLastError());
+    k_in2_shift<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w),
+                                                 (long long)in2_copy_elems(h, w));
     CUDA_TRY(cudaGetLastError());
     return LMT_OK;
 }

@@ -44,6 +44,7 @@ constexpr int U = LMT_U, D = LMT_D;
 constexpr int kMaxStagesJ = 16;
 constexpr int H2 = LMT_H2, W2 = LMT_W2, P2 = LMT_P2;
 constexpr int PF = LMT_PF;
+constexpr long long CS = (long long)(H2 + kIn2PhysHaloRows) * P2;  // floats per in2 copy (lmt_args.h)
 
 // ----------------------------------------------------- stencil (kernel_model.py:115-130)
 __host__ __device__ constexpr bool tap_in(int a, int b) {
@@ -133,21 +134,20 @@ __device__ __forceinline__ void tma_load_2d(float *dst, const TensorMap *map, un
 
 // ----------------------------------------------------- target-array sources
 
-// K1: plain global loads through the read-only path. One uniform base
-// pointer plus a signed 32-bit element offset per work unit (every `in`
-// index is < 2^31, checked on the host).
+// K1: plain global loads through the read-only path. One pointer per work
+// unit; a step adds the (i, j) offset once per work unit and every stencil
+// row once more, the column taps are immediate offsets of one LDG each.
 struct GlobalSrc {
-    const float *base;  // `in` element (PAD, PAD): uniform across the CTA
-    int o[U];           // offset of (home row, home col) of (i=0, j=0), per work unit
+    const float *p[U];  // element (home row, home col) of (i=0, j=0), per work unit
     int pitch;
     template <int NU_>
     __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
         const int step = r * pitch + c;
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
-            const int q = o[u] + step;  // signed: taps above/left of the home element are negative
+            const float *q = p[u] + step;
 #pragma unroll
-            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(base + (q + (tap_dr(k) * pitch + tap_dc(k))));
+            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(q + (tap_dr(k) * pitch + tap_dc(k)));
         }
     }
 };
@@ -224,20 +224,45 @@ __device__ __forceinline__ float ctx_uncoal(const SynthArgs &A, const float *in2
 #endif
 }
 
+// The uncoalesced context reads in2[row][t .. t + N - 1] (N <= 8) as one or
+// two 128-bit loads from the shifted copy (t & 3) (lmt_args.h): `p` points at
+// column t of copy 0.
+template <int N, int CAP>
+__device__ __forceinline__ void uncoal_vec(float (&w)[CAP], const float *p, int t) {
+    if constexpr (N > 0) {
+        const int sh = t & 3;
+        const float4 *v = reinterpret_cast<const float4 *>(p + (sh * CS - sh));
+        const float4 a = __ldg(v);
+        w[0] = a.x;
+        if constexpr (N > 1) w[1] = a.y;
+        if constexpr (N > 2) w[2] = a.z;
+        if constexpr (N > 3) w[3] = a.w;
+        if constexpr (N > 4) {
+            const float4 b = __ldg(v + 1);
+            w[4] = b.x;
+            if constexpr (N > 5) w[5] = b.y;
+            if constexpr (N > 6) w[6] = b.z;
+            if constexpr (N > 7) w[7] = b.w;
+        }
+    }
+}
+
 template <int NU_, class Src>
 __device__ __forceinline__ void fill(Slot<NU_> &s, const Src &src, const Cursor &q, const SynthArgs &A,
                                      const float *in2c, const float *in2u) {
 #if LMT_PF > 0 && !LMT_CTXWRAP
-    // the one new coal row a step touches (rows trow .. trow+NC-1), PF steps
-    // ahead; the uncoal lines only when the walk enters a new 128-byte line
+    // the one new coal row a step touches (rows trow .. trow+NC-1), PF steps ahead
     if (NC > 0) prefetch_l1(q.crow + (NC - 1 + PF) * P2);
-    if (NU > 0 && ((q.tcol + NU - 1 + PF) & 31) == 0) prefetch_l1(q.ucol + (NU - 1 + PF));
 #endif
     src.template load<NU_>(s.v, q.r, q.c);
 #pragma unroll
     for (int k = 0; k < NC; ++k) s.c[k] = ctx_coal(A, in2c, q.crow, q.trow, k);
+#if LMT_CTXWRAP
 #pragma unroll
     for (int k = 0; k < NU; ++k) s.w[k] = ctx_uncoal(A, in2u, q.ucol, q.tcol, k);
+#else
+    uncoal_vec<NU>(s.w, q.ucol, q.tcol);
+#endif
 }
 
 __device__ __forceinline__ void advance(Cursor &q, const SynthArgs &A, const float *in2c, const float *in2u) {
@@ -329,7 +354,11 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, co
 #pragma unroll
     for (int k = 0; k < NCE; ++k) ce[k] = ctx_coal(A, in2c, in2c + (size_t)A.ep_row0 * P2, A.ep_row0, k);
 #pragma unroll
+#if LMT_CTXWRAP
     for (int k = 0; k < NUE; ++k) ue[k] = ctx_uncoal(A, in2u, in2u + A.ep_col0, A.ep_col0, k);
+#else
+    uncoal_vec<NUE>(ue, in2u + A.ep_col0, A.ep_col0);
+#endif
 #pragma unroll
     for (int k = 0; k < CE; ++k)
 #pragma unroll
@@ -363,13 +392,12 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const Synth
     for (; it + U <= nit; it += U) {
         GlobalSrc src;
         src.pitch = A.P;
-        src.base = in0;
         size_t o[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int ix = (it + u) % A.nwx, iy = (it + u) / A.nwx;
             const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
-            src.o[u] = (A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y;
+            src.p[u] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
             o[u] = (size_t)wu_y * A.out_w + wu_x;
         }
         float acc[U];
@@ -382,8 +410,7 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const Synth
         const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
         GlobalSrc src;
         src.pitch = A.P;
-        src.base = in0;
-        src.o[0] = (A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y;
+        src.p[0] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
         float acc[1];
         run_units<1>(A, src, in2c, in2u, acc);
         A.out[(size_t)wu_y * A.out_w + wu_x] = acc[0];

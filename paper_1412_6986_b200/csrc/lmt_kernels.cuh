@@ -370,6 +370,20 @@ __global__ void k_in2_halo(float *__restrict__ buf, int H2, int W2, int P2) {
     }
 }
 
+// Copies 1 .. kIn2Copies-1 of the haloed in2 (see lmt_args.h):
+// copy_s[r][x] = copy_0[r][(x + s) % W2], all rows incl. the halo rows.
+__global__ void k_in2_shift(float *__restrict__ buf, int H2, int W2, int P2, long long copy_elems) {
+    const long long rows = (long long)H2 + kIn2PhysHaloRows;
+    const long long total = rows * P2 * (kIn2Copies - 1);
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
+         v += (long long)gridDim.x * blockDim.x) {
+        const long long cs = v / (rows * P2), rem = v - cs * rows * P2;
+        const long long r = rem / P2, x = rem - r * P2;
+        const int s = (int)cs + 1;
+        buf[(long long)s * copy_elems + rem] = buf[r * P2 + (x + s) % W2];
+    }
+}
+
 // ---------------------------------------------------------------- digest
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
