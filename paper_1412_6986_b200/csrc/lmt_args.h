@@ -30,7 +30,15 @@ struct SynthArgs {
     // generic stencil (radius > 2, AOT kernels only)
     int K;
     signed char sdr[kMaxGenericOffsets], sdc[kMaxGenericOffsets];
+    // floats between the kInCopies shifted copies of `in` (0: one copy only);
+    // copy_s[r][x] = in[r][x + s] (see k_in_shift)
+    long long in_copy;
 };
+
+// Shifted copies of `in` for the baseline's 128-bit loads of stencil rows
+// with >= 5 taps (the row's first tap is read from copy (addr & 3) at a
+// 16-byte-aligned address).
+constexpr int kInCopies = 4;
 
 // in2 is stored with a wrapped halo: physical [IN2_H + 16][P2 >= IN2_W + 8],
 // cell (r, c) = logical in2[r % IN2_H][c % IN2_W]. A context read

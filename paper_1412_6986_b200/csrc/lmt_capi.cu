@@ -240,6 +240,7 @@ struct DevCtx {
     float *in = nullptr;
     size_t in_cap = 0;          // floats
     int64_t in_rows = -1, in_cols = -1, in_pitch = -1;
+    int in_copies = 0;
     float *in2 = nullptr;
     size_t in2_cap = 0;
     int64_t in2_h = -1, in2_w = -1;
@@ -315,6 +316,7 @@ struct Plan {
     bool wide;
     bool jit;           // NVRTC-specialised kernels (lmt_jit.cuh) instead of the AOT set
     JitKey kb, ko;      // their keys (baseline, optimized)
+    int in_copies;      // shifted copies of `in` the baseline reads (1 or kInCopies)
     size_t dyn_smem;
     dim3 grid, block;
     double alg_bytes, alg_flops;
@@ -382,6 +384,11 @@ int jit_pf() {
     const char *e = getenv("LMT_PF");
     const int v = e ? atoi(e) : 8;
     return std::max(0, std::min(v, kPfMax - 1));
+}
+
+bool jit_vec() {
+    const char *e = getenv("LMT_VEC");
+    return !(e && e[0] == '0');
 }
 
 bool jit_enabled() {
@@ -587,7 +594,9 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
                              p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
         JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
                   p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
-                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf()};
+                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf(), 0};
+        // 128-bit stencil-row loads in the baseline need rows of >= 5 taps (radius >= 2)
+        k0.vec = (p.stencil_radius >= 2 && jit_vec()) ? 1 : 0;
         int Ub, Db, Uo, Do, Sb, So;
         choose_jit(K, p, maxt, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
         choose_jit(K, p, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
@@ -603,6 +612,7 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
         pl->u_base = Ub;
         pl->u_opt = Uo;
     }
+    pl->in_copies = (pl->jit && pl->kb.vec) ? kInCopies : 1;
     A.nstages = (int32_t)S;
     pl->dyn_smem = (size_t)S * A.stage_bytes;
     if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
@@ -632,6 +642,7 @@ int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_r
                    const float *d_in2x, float *d_out, cudaStream_t s) {
     Plan pl = pl0;
     pl.A.in = d_in;
+    pl.A.in_copy = pl.in_copies > 1 ? in_rows * pitch : 0;  // d_in holds in_copies shifted copies
     pl.A.in2 = d_in2x;
     pl.A.P2 = (int32_t)in2_pitch(pl.A.W2);
     pl.A.out = d_out;
@@ -682,6 +693,14 @@ int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int sms) {
     CUDA_TRY(cudaGetLastError());
     k_in2_shift<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w),
                                                  (long long)in2_copy_elems(h, w));
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+int launch_in_shift(float *buf, int64_t rows, int64_t pitch, cudaStream_t s, int sms) {
+    const int64_t total = rows * pitch * (kInCopies - 1);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 16));
+    k_in_shift<<<(unsigned)blocks, 256, 0, s>>>(buf, rows, pitch);
     CUDA_TRY(cudaGetLastError());
     return LMT_OK;
 }
@@ -764,7 +783,16 @@ int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, co
     CUDA_TRY(cudaMemcpy2DAsync(x, (size_t)in2_pitch(inst->in_w) * 4, d_in2, (size_t)inst->in_w * 4,
                                (size_t)inst->in_w * 4, (size_t)inst->in_h, cudaMemcpyDeviceToDevice, s));
     rc = launch_in2_halo(x, inst->in_h, inst->in_w, s, c->sms);
-    if (rc == LMT_OK) rc = launch_variant(pl, variant, d_in, in_rows, in_cols, in_pitch, x, d_out, s);
+    // the baseline's 128-bit row loads read shifted copies of `in`: stage them too
+    float *xin = nullptr;
+    if (rc == LMT_OK && variant == 0 && pl.in_copies > 1) {
+        const size_t n = (size_t)in_rows * (size_t)in_pitch;
+        CUDA_TRY(cudaMallocAsync(&xin, (n * pl.in_copies + 64) * sizeof(float), s));
+        CUDA_TRY(cudaMemcpyAsync(xin, d_in, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        rc = launch_in_shift(xin, in_rows, in_pitch, s, c->sms);
+    }
+    if (rc == LMT_OK) rc = launch_variant(pl, variant, xin ? xin : d_in, in_rows, in_cols, in_pitch, x, d_out, s);
+    if (xin) CUDA_TRY(cudaFreeAsync(xin, s));
     CUDA_TRY(cudaFreeAsync(x, s));
     return rc;
 }
@@ -845,10 +873,11 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
                              : pl.sid * 100 + (pl.wide ? 50 : 0) + pl.u_base * 10 + pl.u_opt;
         cudaEvent_t *ev = &c->events[(size_t)i * 4];
         // ---- inputs (make_inputs, interp.py:30-38)
-        const size_t need_in = (size_t)(rows * pitch), need_out = (size_t)p.out_h * p.out_w;
+        const size_t need_in = (size_t)(rows * pitch) * pl.in_copies + 64, need_out = (size_t)p.out_h * p.out_w;
         const size_t need_in2 = in2_phys_elems(p.in_h, p.in_w);
         const int64_t p2 = in2_pitch(p.in_w);
-        if (host || c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in) {
+        if (host || c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in ||
+            c->in_copies < pl.in_copies) {
             if (need_in > c->in_cap) {
                 CUDA_TRY(cudaStreamSynchronize(s));
                 size_t fr = 0, tot = 0;
@@ -869,6 +898,12 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
                 if (rc) return rc;
             }
             m.launches += host ? 0 : 1;
+            if (pl.in_copies > 1) {
+                rc = launch_in_shift(c->in, rows, pitch, s, c->sms);
+                if (rc) return rc;
+                m.launches += 1;
+            }
+            c->in_copies = pl.in_copies;
             c->in_rows = host ? -1 : rows;
             c->in_cols = host ? -1 : cols;
             c->in_pitch = host ? -1 : pitch;

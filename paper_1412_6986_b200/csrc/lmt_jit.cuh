@@ -31,6 +31,7 @@
 //   LMT_OPT                              0 baseline (global loads), 1 optimized (TMA -> smem)
 //   LMT_WIDE                             optimized variant with several 256-column TMA chunks
 //   LMT_CTXWRAP                          context counts exceed the in2 halo: reduce indices mod IN2_H/W
+//   LMT_VEC                              baseline: 128-bit loads for stencil rows of >= 5 taps
 //   LMT_PF                               L1 prefetch distance in steps for the in2 context lines (0 off)
 //   LMT_H2 LMT_W2 LMT_P2                 in2 shape (IN2_H, IN2_W: #defines in the reference too) and
 //                                        its physical pitch, so every context read of a step is
@@ -134,12 +135,28 @@ __device__ __forceinline__ void tma_load_2d(float *dst, const TensorMap *map, un
 
 // ----------------------------------------------------- target-array sources
 
+// Row structure of the stencil: half-width of row dr and index of its
+// first tap (taps are row-major, dc ascending).
+__host__ __device__ constexpr int row_w(int dr) {
+    return SHAPE == 0 ? RAD : SHAPE == 1 ? RAD - (dr < 0 ? -dr : dr) : (dr == 0 ? RAD : 0);
+}
+__host__ __device__ constexpr int row_first(int dr) {
+    int k = 0;
+    for (int a = -RAD; a < dr; ++a) k += 2 * row_w(a) + 1;
+    return k;
+}
+
 // K1: plain global loads through the read-only path. One pointer per work
 // unit; a step adds the (i, j) offset once per work unit and every stencil
-// row once more, the column taps are immediate offsets of one LDG each.
+// row once more. Rows of >= 5 taps are read with 128-bit loads (LMT_VEC):
+// the row's first tap lives at a 16-byte-aligned address of shifted copy
+// (addr & 3) of `in` (k_in_shift), so ceil(taps / 4) LDG.128 replace the
+// scalar loads -- the "coalesced, vectorised (128-bit) global loads" of the
+// baseline, fewer L1 wavefronts when the lanes of a warp walk different rows.
 struct GlobalSrc {
     const float *p[U];  // element (home row, home col) of (i=0, j=0), per work unit
     int pitch;
+    long long cs;       // floats between copies of `in`
     template <int NU_>
     __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
         const int step = r * pitch + c;
@@ -147,7 +164,25 @@ struct GlobalSrc {
         for (int u = 0; u < NU_; ++u) {
             const float *q = p[u] + step;
 #pragma unroll
-            for (int k = 0; k < KT; ++k) v[u][k] = __ldg(q + (tap_dr(k) * pitch + tap_dc(k)));
+            for (int dr = -RAD; dr <= RAD; ++dr) {
+                const int w = row_w(dr), k0 = row_first(dr), nt = 2 * w + 1;
+                if (LMT_VEC && nt >= 5) {
+                    const float *st = q + (dr * pitch - w);
+                    const int sh = (int)(reinterpret_cast<unsigned long long>(st) >> 2) & 3;
+                    const float4 *vp = reinterpret_cast<const float4 *>(st + ((long long)sh * cs - sh));
+#pragma unroll
+                    for (int b = 0; b < (nt + 3) / 4; ++b) {
+                        const float4 x = __ldg(vp + b);
+                        if (4 * b + 0 < nt) v[u][k0 + 4 * b + 0] = x.x;
+                        if (4 * b + 1 < nt) v[u][k0 + 4 * b + 1] = x.y;
+                        if (4 * b + 2 < nt) v[u][k0 + 4 * b + 2] = x.z;
+                        if (4 * b + 3 < nt) v[u][k0 + 4 * b + 3] = x.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < nt; ++t) v[u][k0 + t] = __ldg(q + (dr * pitch + t - w));
+                }
+            }
         }
     }
 };
@@ -353,8 +388,8 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, co
     float ce[NCE > 0 ? NCE : 1], ue[NUE > 0 ? NUE : 1];
 #pragma unroll
     for (int k = 0; k < NCE; ++k) ce[k] = ctx_coal(A, in2c, in2c + (size_t)A.ep_row0 * P2, A.ep_row0, k);
-#pragma unroll
 #if LMT_CTXWRAP
+#pragma unroll
     for (int k = 0; k < NUE; ++k) ue[k] = ctx_uncoal(A, in2u, in2u + A.ep_col0, A.ep_col0, k);
 #else
     uncoal_vec<NUE>(ue, in2u + A.ep_col0, A.ep_col0);
@@ -392,6 +427,7 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const Synth
     for (; it + U <= nit; it += U) {
         GlobalSrc src;
         src.pitch = A.P;
+        src.cs = A.in_copy;
         size_t o[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -410,6 +446,7 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const Synth
         const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
         GlobalSrc src;
         src.pitch = A.P;
+        src.cs = A.in_copy;
         src.p[0] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
         float acc[1];
         run_units<1>(A, src, in2c, in2u, acc);

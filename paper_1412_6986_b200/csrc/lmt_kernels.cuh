@@ -384,6 +384,19 @@ __global__ void k_in2_shift(float *__restrict__ buf, int H2, int W2, int P2, lon
     }
 }
 
+// Copies 1 .. kInCopies-1 of `in` ([rows][P], copy stride rows*P floats):
+// copy_s[r][x] = in[r][x + s] within the row (0 past it).
+__global__ void k_in_shift(float *__restrict__ buf, long long rows, long long P) {
+    const long long n = rows * P;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n * (kInCopies - 1);
+         v += (long long)gridDim.x * blockDim.x) {
+        const long long cs = v / n, rem = v - cs * n;
+        const long long r = rem / P, x = rem - r * P;
+        const int s = (int)cs + 1;
+        buf[(long long)s * n + rem] = (x + s < P) ? buf[r * P + x + s] : 0.0f;
+    }
+}
+
 // ---------------------------------------------------------------- digest
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
