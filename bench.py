@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rf", action="store_true")
+    ap.add_argument("--no-real", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dump", default=None, help="save per-instance records and measurements (npz)")
     return ap.parse_args()
@@ -290,6 +291,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.no_e2e:
         e2e = run_e2e(args, L, table, perm, world, rank, barrier)
     rf = None if args.no_rf else run_rf(args, L, world, rank, barrier)
+    real = None if (args.no_real or rank != 0) else run_real(args, L, hbm_peak, fp32_peak)
 
     if rank != 0:
         return
@@ -330,9 +332,47 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         line["e2e"] = e2e
     if rf:
         line["rf"] = rf
+    if real:
+        line["real_kernels"] = real
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def run_real(args, L, hbm_peak: float, fp32_peak: float):
+    """BASELINE config 2: the real-kernel set (transpose, matrixMul,
+    convolution-separable, MVT; K5) in both variants on this GPU, one warm-up
+    pass then one measured pass; per kernel the best launch of each variant on
+    its roof (transpose/convolution/MVT: HBM bytes; matrixMul: fp32 flops)."""
+    R = L.real
+    insts = R.instance_set()
+    R.measure(insts)  # warm-up
+    ms = R.measure(insts)
+    out = {"instances": len(insts), "verified_bitwise": int((ms["mismatches"] == 0).sum()),
+           "sizes": {"transpose": 2048, "matrixMul": 1024, "convolution-separable": 2048, "MVT": 4096}}
+    for k, name in enumerate(R.KERNELS):
+        sel = np.array([i.kernel == k for i in insts])
+        m = ms[sel]
+        sub = [i for i in insts if i.kernel == k]
+        entry = {"instances": int(sel.sum())}
+        for col, var in (("t_base_ms", "baseline"), ("t_opt_ms", "optimized")):
+            j = int(np.argmin(m[col]))
+            t = float(m[col][j]) / 1e3
+            i = sub[j]
+            if k == 1:
+                entry[var] = {"best_ms": t * 1e3, "tflops": m["alg_flops"][j] / t / 1e12,
+                              "frac": m["alg_flops"][j] / t / 1e12 / fp32_peak,
+                              "config": f"tile {i.tile} wg {i.wg_x}x{i.wg_y}"}
+            else:
+                entry[var] = {"best_ms": t * 1e3, "gbs": m["alg_bytes"][j] / t / 1e9,
+                              "frac": m["alg_bytes"][j] / t / 1e9 / hbm_peak,
+                              "config": f"wg {i.wg_x}x{i.wg_y}" + (f" tile {i.tile}" if i.tile else "")
+                                        + (f" radius {i.radius}" if i.radius else "")}
+        sp = m["t_base_ms"] / m["t_opt_ms"]
+        entry["speedup_opt_over_base"] = {"min": float(sp.min()), "median": float(np.median(sp)),
+                                          "max": float(sp.max())}
+        out[name] = entry
+    return out
 
 
 def run_rf(args, L, world, rank, barrier):

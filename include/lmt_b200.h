@@ -184,6 +184,27 @@ int lmt_features(const lmt_instance *insts, int64_t n, const lmt_device *devs, i
                  const double *coal_override, const int64_t *lmem_override, double *h_X,
                  double *h_label, double *h_times, int32_t *h_status);
 
+/* K5: the real-world kernel set of the paper (BASELINE.json
+ * configs[1]) in both variants. The reference has no implementation of it
+ * (SPEC.md:15); semantics are defined in csrc/lmt_real.cuh and pinned by the
+ * C oracle. kernel: 0 transpose, 1 matrixMul, 2 convolution-separable,
+ * 3 MVT. tile: transpose / matrixMul tile (== wg_x; wg_y = tile / work per
+ * thread), MVT j-tile; radius: convolution radius (1..16). */
+typedef struct lmt_real_instance {
+    int32_t kernel, n, wg_x, wg_y, tile, radius;
+} lmt_real_instance;
+
+/* 0 when valid, else 1 with the reason in msg. */
+int lmt_real_validate(const lmt_real_instance *inst, char *msg, int64_t cap);
+/* One variant on caller buffers: inputs transpose {A}, matrixMul {A, B},
+ * convolution {in}, MVT {A, y1, y2, x1_0, x2_0}; d_out n*n floats (MVT: 2n,
+ * x1 then x2). Asynchronous on `stream`. */
+int lmt_real_execute(const lmt_real_instance *inst, int variant, const float *const *d_inputs, float *d_out,
+                     void *stream);
+/* Hash-filled inputs, both variants timed with CUDA events, outputs digested
+ * and compared bitwise on the device (same record as lmt_measure_batch). */
+int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, lmt_measurement *out);
+
 /* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
  * compiles) and the host seconds spent compiling. */
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);

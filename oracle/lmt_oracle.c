@@ -415,3 +415,76 @@ int ora_forest_mean(const int32_t *feature, const double *threshold,
     for (int t = 0; t < nthreads; t++) pthread_join(tids[t], NULL);
     return ORA_OK;
 }
+
+/* ------------------------------------------------------------ K5 real kernels */
+
+void ora_real_transpose(const float *A, float *B, int64_t n) {
+    for (int64_t y = 0; y < n; y++)
+        for (int64_t x = 0; x < n; x++) B[x * n + y] = A[y * n + x];
+}
+
+typedef struct {
+    const float *A, *B;
+    float *C;
+    int64_t n;
+    int tid, nt;
+} mm_ctx;
+
+static void *mm_worker(void *arg) {
+    mm_ctx *c = (mm_ctx *)arg;
+    for (int64_t i = c->tid; i < c->n; i += c->nt)
+        for (int64_t j = 0; j < c->n; j++) {
+            float acc = 0.0f;
+            for (int64_t k = 0; k < c->n; k++) acc = fmaf(c->A[i * c->n + k], c->B[k * c->n + j], acc);
+            c->C[i * c->n + j] = acc;
+        }
+    return NULL;
+}
+
+void ora_real_matmul(const float *A, const float *B, float *C, int64_t n, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t t[256];
+    mm_ctx c[256];
+    for (int k = 0; k < nthreads; k++) {
+        c[k] = (mm_ctx){A, B, C, n, k, nthreads};
+        pthread_create(&t[k], NULL, mm_worker, &c[k]);
+    }
+    for (int k = 0; k < nthreads; k++) pthread_join(t[k], NULL);
+}
+
+/* rows: tmp[y][x] = sum_{k=-R..R} in[y][x+k] * w[R-k]; cols: out[y][x] = sum_k tmp[y+k][x] * w[R-k];
+ * taps outside the image read 0 (the fmaf still happens, like the kernels). */
+void ora_real_conv(const float *in, float *tmp, float *out, int64_t n, int R, const float *w) {
+    for (int64_t y = 0; y < n; y++)
+        for (int64_t x = 0; x < n; x++) {
+            float acc = 0.0f;
+            for (int k = -R; k <= R; k++) {
+                const int64_t xx = x + k;
+                acc = fmaf((xx >= 0 && xx < n) ? in[y * n + xx] : 0.0f, w[R - k], acc);
+            }
+            tmp[y * n + x] = acc;
+        }
+    for (int64_t y = 0; y < n; y++)
+        for (int64_t x = 0; x < n; x++) {
+            float acc = 0.0f;
+            for (int k = -R; k <= R; k++) {
+                const int64_t yy = y + k;
+                acc = fmaf((yy >= 0 && yy < n) ? tmp[yy * n + x] : 0.0f, w[R - k], acc);
+            }
+            out[y * n + x] = acc;
+        }
+}
+
+void ora_real_mvt(const float *A, const float *y1, const float *y2, const float *x1_0, const float *x2_0,
+                  float *x1, float *x2, int64_t n) {
+    for (int64_t i = 0; i < n; i++) {
+        float a1 = x1_0[i], a2 = x2_0[i];
+        for (int64_t j = 0; j < n; j++) {
+            a1 = fmaf(A[i * n + j], y1[j], a1);
+            a2 = fmaf(A[j * n + i], y2[j], a2);
+        }
+        x1[i] = a1;
+        x2[i] = a2;
+    }
+}

@@ -79,6 +79,15 @@ int ora_forest_mean(const int32_t *feature, const double *threshold,
                     const double *X, int64_t nrows, int32_t nfeat, double *mean_out,
                     int nthreads);
 
+/* K5 real-kernel set (paper Table 3; semantics of csrc/lmt_real.cuh, which the
+ * reference does not implement: parity is pinned by this restatement, not by
+ * reference outputs). Accumulation order k / j / tap ascending with fmaf. */
+void ora_real_transpose(const float *A, float *B, int64_t n);
+void ora_real_matmul(const float *A, const float *B, float *C, int64_t n, int nthreads);
+void ora_real_conv(const float *in, float *tmp, float *out, int64_t n, int radius, const float *w);
+void ora_real_mvt(const float *A, const float *y1, const float *y2, const float *x1_0, const float *x2_0,
+                  float *x1, float *x2, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,10 @@ class CGeometry(ctypes.Structure):
     ]
 
 
+class CRealInstance(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in ("kernel", "n", "wg_x", "wg_y", "tile", "radius")]
+
+
 class CMeasurement(ctypes.Structure):
     _fields_ = [
         ("t_base_ms", ctypes.c_double), ("t_opt_ms", ctypes.c_double),
@@ -78,7 +82,8 @@ EXPORTS = (
     "lmt_version", "lmt_last_error", "lmt_validate", "lmt_emit_geometry", "lmt_fill",
     "lmt_execute", "lmt_measure_batch", "lmt_measure_batch_host", "lmt_digest",
     "lmt_rf_create", "lmt_rf_mean", "lmt_rf_mean_host", "lmt_rf_destroy", "lmt_sync",
-    "lmt_get_stream", "lmt_prepare", "lmt_jit_stats", "lmt_features",
+    "lmt_get_stream", "lmt_prepare", "lmt_jit_stats", "lmt_features", "lmt_real_validate",
+    "lmt_real_execute", "lmt_real_measure",
 )
 
 _lib = None
@@ -111,6 +116,9 @@ def _declare(L):
     L.lmt_get_stream.argtypes = [P(vp)]
     L.lmt_prepare.argtypes = [P(CInstance), c_i64, P(CDevice), c_i32, c_i32, P(c_i64)]
     L.lmt_jit_stats.argtypes = [P(c_i64), P(ctypes.c_double)]
+    L.lmt_real_validate.argtypes = [P(CRealInstance), ctypes.c_char_p, c_i64]
+    L.lmt_real_execute.argtypes = [P(CRealInstance), ctypes.c_int, P(vp), vp, vp]
+    L.lmt_real_measure.argtypes = [P(CRealInstance), c_i64, c_i32, P(CMeasurement)]
     L.lmt_features.argtypes = [P(CInstance), c_i64, P(CDevice), c_i64, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         fn = getattr(L, name)

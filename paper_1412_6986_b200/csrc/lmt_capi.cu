@@ -20,6 +20,7 @@
 #include "lmt_synth_ilp.cuh"
 #include "lmt_jit_host.cuh"
 #include "lmt_features.cuh"
+#include "lmt_real.cuh"
 
 #ifndef LMT_VERSION
 #define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
@@ -1107,6 +1108,255 @@ int lmt_features(const lmt_instance *insts, int64_t n, const lmt_device *devs, i
     CUDA_TRY(cudaMemcpyAsync(h_status, d_s, bs, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaFreeAsync(buf, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    return LMT_OK;
+}
+
+// ------------------------------------------------------------ K5 real kernels
+
+namespace {
+
+const uint32_t kRealSalt[8] = {21, 22, 23, 24, 25, 26, 27, 28};  // A, B, conv in, y1, y2, x1_0, x2_0, w
+
+std::string real_violations(const lmt_real_instance &r) {
+    char b[256];
+    const int64_t n = r.n, wx = r.wg_x, wy = r.wg_y, T = r.tile;
+    if (n < 1) return "n < 1";
+    if (wx < 1 || wy < 1 || wx * wy > 1024) { snprintf(b, sizeof b, "workgroup %lldx%lld", (long long)wx, (long long)wy); return b; }
+    switch (r.kernel) {
+        case 0:
+            if (T != wx || T > 32 || T % wy || n % T) return "transpose needs tile == wg_x <= 32, wg_y | tile, tile | n";
+            return "";
+        case 1:
+            if (T != wx || T > 32 || T % wy || n % T) return "matrixMul needs tile == wg_x <= 32, wg_y | tile, tile | n";
+            if (T / wy != 1 && T / wy != 2 && T / wy != 4 && T / wy != 8) return "matrixMul work per thread tile/wg_y must be 1, 2, 4 or 8";
+            return "";
+        case 2:
+            if (n % wx || n % wy) return "convolution needs wg_x | n and wg_y | n";
+            if (r.radius < 1 || r.radius > kConvMaxRadius) return "convolution radius must be in [1, 16]";
+            return "";
+        case 3:
+            if (wy != 1 || n % wx || T < 1 || n % T) return "MVT needs wg_y == 1, wg_x | n, tile | n";
+            return "";
+        default:
+            return "unknown real kernel";
+    }
+}
+
+double real_hash(uint64_t idx) {  // interp._hash_fill's value, on the host (exact double math)
+    const uint32_t v = (uint32_t)(idx * 2654435761ull);
+    return (double)(float)((double)v / 4294967296.0 - 0.5);
+}
+
+RealConv real_weights(int R) {
+    RealConv c{};
+    for (int k = 0; k <= 2 * R; k++) c.w[k] = (float)real_hash((uint64_t)k + kRealSalt[7]);
+    return c;
+}
+
+// inputs: transpose {A}; matrixMul {A, B}; convolution {in} (+ scratch `tmp`
+// of n*n floats); MVT {A, y1, y2, x1_0, x2_0}; out: n*n floats, MVT 2n (x1 then x2)
+int real_launch(const lmt_real_instance &r, int variant, const float *const *in, float *out, float *tmp,
+                cudaStream_t s, int smem_optin) {
+    const int n = r.n, wx = r.wg_x, wy = r.wg_y, T = r.tile;
+    const dim3 blk(wx, wy);
+    switch (r.kernel) {
+        case 0: {
+            const dim3 grd(n / T, n / T);
+            if (variant == 0) k_transpose_base<<<grd, blk, 0, s>>>(in[0], out, n, T);
+            else k_transpose_opt<<<grd, blk, (size_t)T * (T + 1) * 4, s>>>(in[0], out, n, T);
+            break;
+        }
+        case 1: {
+            const dim3 grd(n / T, n / T);
+            const int W = T / wy;
+            if (variant == 0) { k_matmul_base<<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W); break; }
+            const size_t sm = (size_t)2 * T * (T + 1) * 4;
+            if (W == 1) k_matmul_opt<1><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
+            else if (W == 2) k_matmul_opt<2><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
+            else if (W == 4) k_matmul_opt<4><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
+            else k_matmul_opt<8><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
+            break;
+        }
+        case 2: {
+            const dim3 grd(n / wx, n / wy);
+            const RealConv c = real_weights(r.radius);
+            const int R = r.radius;
+            if (variant == 0) {
+                k_conv_rows_base<<<grd, blk, 0, s>>>(in[0], tmp, n, R, c);
+                k_conv_cols_base<<<grd, blk, 0, s>>>(tmp, out, n, R, c);
+            } else {
+                k_conv_rows_opt<<<grd, blk, (size_t)wy * (wx + 2 * R) * 4, s>>>(in[0], tmp, n, R, c);
+                k_conv_cols_opt<<<grd, blk, (size_t)(wy + 2 * R) * wx * 4, s>>>(tmp, out, n, R, c);
+            }
+            break;
+        }
+        case 3: {
+            const dim3 grd(n / wx);
+            if (variant == 0) {
+                k_mvt1_base<<<grd, wx, 0, s>>>(in[0], in[1], in[3], out, n);
+                k_mvt2_base<<<grd, wx, 0, s>>>(in[0], in[2], in[4], out + n, n);
+            } else {
+                const size_t sm1 = ((size_t)wx * (T + 1) + T) * 4;
+                if ((int64_t)sm1 > smem_optin - 1024) return fail(LMT_ERR_TOO_LARGE, "MVT tile needs %zu bytes of shared memory", sm1);
+                k_mvt1_opt<<<grd, wx, sm1, s>>>(in[0], in[1], in[3], out, n, T);
+                k_mvt2_opt<<<grd, wx, (size_t)T * 4, s>>>(in[0], in[2], in[4], out + n, n, T);
+            }
+            break;
+        }
+    }
+    CUDA_TRY(cudaGetLastError());
+    return LMT_OK;
+}
+
+void real_work(const lmt_real_instance &r, double *bytes, double *flops) {
+    const double n = r.n;
+    switch (r.kernel) {
+        case 0: *bytes = 8.0 * n * n; *flops = 0.0; break;
+        case 1: *bytes = 12.0 * n * n; *flops = 2.0 * n * n * n; break;
+        case 2: *bytes = 16.0 * n * n; *flops = 4.0 * (2 * r.radius + 1) * n * n; break;
+        default: *bytes = 8.0 * n * n + 24.0 * n; *flops = 4.0 * n * n; break;
+    }
+}
+
+struct RealBufs {
+    int64_t n = -1;
+    float *in[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    float *tmp = nullptr, *ob = nullptr, *oo = nullptr;
+    unsigned long long *dres = nullptr;
+} g_real[64];
+
+int real_attrs_once(int smem_optin) {
+    static bool done = false;
+    if (done) return LMT_OK;
+    const int cap = smem_optin - 1024;
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_opt), cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_rows_opt), cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_cols_opt), cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    done = true;
+    return LMT_OK;
+}
+
+}  // namespace
+
+int lmt_real_validate(const lmt_real_instance *inst, char *msg, int64_t cap) {
+    if (!inst) return -1;
+    const std::string v = real_violations(*inst);
+    if (msg && cap > 0) snprintf(msg, (size_t)cap, "%s", v.c_str());
+    return v.empty() ? 0 : 1;
+}
+
+int lmt_real_execute(const lmt_real_instance *inst, int variant, const float *const *d_inputs, float *d_out,
+                     void *stream) {
+    if (!inst || !d_inputs || !d_out || (variant != 0 && variant != 1)) return fail(LMT_ERR_ARG, "bad real arguments");
+    const std::string v = real_violations(*inst);
+    if (!v.empty()) return fail(LMT_ERR_INVALID_INSTANCE, "%s", v.c_str());
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    if ((rc = real_attrs_once((int)c->smem_optin))) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    float *tmp = nullptr;
+    if (inst->kernel == 2) CUDA_TRY(cudaMallocAsync(&tmp, (size_t)inst->n * inst->n * 4, s));
+    rc = real_launch(*inst, variant, d_inputs, d_out, tmp, s, (int)c->smem_optin);
+    if (tmp) CUDA_TRY(cudaFreeAsync(tmp, s));
+    return rc;
+}
+
+int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, lmt_measurement *out) {
+    if ((!insts && n > 0) || !out || n < 0) return fail(LMT_ERR_ARG, "bad real measure arguments");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    if ((rc = real_attrs_once((int)c->smem_optin))) return rc;
+    RealBufs &B = g_real[c->device];
+    cudaStream_t s = c->stream;
+    std::vector<cudaEvent_t> ev((size_t)n * 3);
+    for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
+    if (!B.dres) CUDA_TRY(cudaMalloc(&B.dres, 3 * sizeof(unsigned long long) * 4096));
+    std::vector<char> ran((size_t)n, 0);
+    std::vector<unsigned long long> res((size_t)n * 3, 0);
+    for (int64_t i = 0; i < n; i++) {
+        lmt_measurement &m = out[i];
+        memset(&m, 0, sizeof m);
+        m.t_opt_ms = -1.0;
+        m.mismatches = -1;
+        const lmt_real_instance &r = insts[i];
+        const std::string v = real_violations(r);
+        if (!v.empty()) { m.status = fail(LMT_ERR_INVALID_INSTANCE, "%s", v.c_str()); continue; }
+        const int64_t N = r.n;
+        if (B.n != N) {  // (re)generate the hashed inputs of this size
+            CUDA_TRY(cudaStreamSynchronize(s));
+            for (auto *p : {&B.in[0], &B.in[1], &B.in[2], &B.in[3], &B.in[4], &B.tmp, &B.ob, &B.oo})
+                if (*p) { CUDA_TRY(cudaFree(*p)); *p = nullptr; }
+            const size_t nn = (size_t)N * N;
+            CUDA_TRY(cudaMalloc(&B.in[0], nn * 4));
+            CUDA_TRY(cudaMalloc(&B.in[1], nn * 4));
+            CUDA_TRY(cudaMalloc(&B.tmp, nn * 4));
+            CUDA_TRY(cudaMalloc(&B.ob, nn * 4 + 8 * N));
+            CUDA_TRY(cudaMalloc(&B.oo, nn * 4 + 8 * N));
+            for (int k = 2; k < 5; k++) CUDA_TRY(cudaMalloc(&B.in[k], (size_t)N * 4 + 16));
+            B.n = N;
+        }
+        // the inputs of this kernel (salts per array; the conv input shares the A buffer slot 0)
+        const size_t nn = (size_t)N * N;
+        if (r.kernel == 2) {
+            rc = launch_fill(B.in[0], N, N, N, kRealSalt[2], s, c->sms);
+        } else {
+            rc = launch_fill(B.in[0], N, N, N, kRealSalt[0], s, c->sms);
+            if (!rc && r.kernel == 1) rc = launch_fill(B.in[1], N, N, N, kRealSalt[1], s, c->sms);
+            if (!rc && r.kernel == 3) {
+                for (int k = 0; k < 4 && !rc; k++)
+                    rc = launch_fill(B.in[1 + k], 1, N, (N + 3) / 4 * 4, kRealSalt[3 + k], s, c->sms);
+            }
+        }
+        if (rc) return rc;
+        const float *ins[5] = {B.in[0], B.in[1], B.in[2], B.in[3], B.in[4]};
+        if (r.kernel == 3) { ins[1] = B.in[1]; ins[2] = B.in[2]; ins[3] = B.in[3]; ins[4] = B.in[4]; }
+        real_work(r, &m.alg_bytes, &m.alg_flops);
+        cudaEvent_t *e = &ev[(size_t)i * 3];
+        CUDA_TRY(cudaEventRecord(e[0], s));
+        rc = real_launch(r, 0, ins, B.ob, B.tmp, s, (int)c->smem_optin);
+        if (rc) { m.status = rc; continue; }
+        CUDA_TRY(cudaEventRecord(e[1], s));
+        m.launches = r.kernel >= 2 ? 2 : 1;
+        const bool run_opt = !(flags & LMT_MEASURE_SKIP_OPT);
+        if (run_opt) {
+            rc = real_launch(r, 1, ins, B.oo, B.tmp, s, (int)c->smem_optin);
+            if (rc) { m.status = rc; continue; }
+            CUDA_TRY(cudaEventRecord(e[2], s));
+            m.launches *= 2;
+        }
+        const int64_t count = r.kernel == 3 ? 2 * N : (int64_t)nn;
+        const size_t slot = (size_t)(i % 4096) * 3;
+        CUDA_TRY(cudaMemsetAsync(B.dres + slot, 0, 3 * sizeof(unsigned long long), s));
+        rc = launch_digest(B.ob, run_opt ? B.oo : nullptr, count, B.dres + slot, s, c->sms);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(&res[(size_t)i * 3], B.dres + slot, 3 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        m.launches += 1;
+        m.kernel_id = 50000 + r.kernel;
+        ran[(size_t)i] = run_opt ? 2 : 1;
+        if ((i + 1) % 4096 == 0) CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n; i++) {
+        if (!ran[(size_t)i]) continue;
+        lmt_measurement &m = out[i];
+        cudaEvent_t *e = &ev[(size_t)i * 3];
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e[0], e[1]));
+        m.t_base_ms = ms;
+        m.digest_base = res[(size_t)i * 3];
+        if (ran[(size_t)i] == 2) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, e[1], e[2]));
+            m.t_opt_ms = ms;
+            m.digest_opt = res[(size_t)i * 3 + 1];
+            m.mismatches = (int64_t)res[(size_t)i * 3 + 2];
+        }
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
     return LMT_OK;
 }
 

@@ -1,0 +1,204 @@
+// lmt_real.cuh -- K5: the real-world kernel set of the paper's Table 3
+// that BASELINE.json configs[1] times on one GPU:
+// transpose, matrixMul (NVIDIA SDK), convolution-separable (SDK) and MVT
+// (Polybench), each as a baseline (plain global loads) and an optimized
+// variant (the reused tile staged in shared memory), as in the paper's study.
+// The reference has no implementation of these; the semantics
+// below are this repository's and are pinned by the C oracle
+// (oracle/lmt_oracle.c ora_real_*), bit for bit.
+//
+// Numerics: every multiply-add is one fmaf (FFMA) and both variants
+// accumulate in the same order (k / j / tap ascending), so baseline,
+// optimized and oracle agree bitwise. Convolution taps outside the image
+// read 0 in all three (the optimized variant's apron is zero-filled).
+// No tensor cores (north_star): these are fp32 CUDA-core kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace lmt {
+
+constexpr int kConvMaxRadius = 16;
+
+struct RealConv {
+    float w[2 * kConvMaxRadius + 1];
+};
+
+// ------------------------------------------------------------ transpose
+// B[x][y] = A[y][x], n x n. CTA = one T x T tile, blockDim (T, wy); each
+// thread walks T / wy rows of the tile (SDK transposeNaive / transposeCoalesced).
+__global__ void k_transpose_base(const float *__restrict__ A, float *__restrict__ B, int n, int T) {
+    const int x = blockIdx.x * T + threadIdx.x;
+    for (int j = threadIdx.y; j < T; j += blockDim.y) {
+        const int y = blockIdx.y * T + j;
+        B[(size_t)x * n + y] = A[(size_t)y * n + x];  // coalesced read, strided write
+    }
+}
+
+__global__ void k_transpose_opt(const float *__restrict__ A, float *__restrict__ B, int n, int T) {
+    extern __shared__ float tile[];  // [T][T + 1]: the +1 makes column reads bank-conflict free
+    const int P = T + 1;
+    const int tx = threadIdx.x;
+    for (int j = threadIdx.y; j < T; j += blockDim.y)
+        tile[j * P + tx] = A[(size_t)(blockIdx.y * T + j) * n + blockIdx.x * T + tx];
+    __syncthreads();
+    for (int j = threadIdx.y; j < T; j += blockDim.y)
+        B[(size_t)(blockIdx.x * T + j) * n + blockIdx.y * T + tx] = tile[tx * P + j];  // coalesced write
+}
+
+// ------------------------------------------------------------ matrixMul
+// C = A x B, n x n. CTA = T x T outputs, blockDim (T, T / W): thread (tx, ty)
+// computes rows ty + r * (T / W), r < W, column tx. acc = fmaf(A[i][k], B[k][j], acc), k ascending.
+__global__ void k_matmul_base(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
+                              int n, int T, int W) {
+    const int h = T / W;
+    const int col = blockIdx.x * T + threadIdx.x;
+    for (int r = 0; r < W; ++r) {
+        const int row = blockIdx.y * T + threadIdx.y + r * h;
+        float acc = 0.0f;
+        for (int k = 0; k < n; ++k) acc = __fmaf_rn(A[(size_t)row * n + k], B[(size_t)k * n + col], acc);
+        C[(size_t)row * n + col] = acc;
+    }
+}
+
+template <int W>
+__global__ void k_matmul_opt(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
+                             int n, int T) {
+    extern __shared__ float sm[];  // As[T][T + 1], Bs[T][T + 1]
+    const int P = T + 1, h = T / W;
+    float *As = sm, *Bs = sm + T * P;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int col = blockIdx.x * T + tx;
+    float acc[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) acc[r] = 0.0f;
+    for (int k0 = 0; k0 < n; k0 += T) {
+#pragma unroll
+        for (int r = 0; r < W; ++r) {
+            const int lr = ty + r * h;
+            As[lr * P + tx] = A[(size_t)(blockIdx.y * T + lr) * n + k0 + tx];
+            Bs[lr * P + tx] = B[(size_t)(k0 + lr) * n + col];
+        }
+        __syncthreads();
+        for (int kk = 0; kk < T; ++kk) {
+            const float b = Bs[kk * P + tx];
+#pragma unroll
+            for (int r = 0; r < W; ++r) acc[r] = __fmaf_rn(As[(ty + r * h) * P + kk], b, acc[r]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < W; ++r) C[(size_t)(blockIdx.y * T + ty + r * h) * n + col] = acc[r];
+}
+
+// ------------------------------------------------------------ convolution-separable
+// rows: out[y][x] = sum_{k=-R..R} in[y][x+k] * w[R-k]; cols: out[y][x] = sum_k in[y+k][x] * w[R-k];
+// taps outside the image read 0; blockDim (wx, wy), one output per thread.
+__global__ void k_conv_rows_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+    float acc = 0.0f;
+    for (int k = -R; k <= R; ++k) {
+        const int xx = x + k;
+        const float v = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
+        acc = __fmaf_rn(v, c.w[R - k], acc);
+    }
+    out[(size_t)y * n + x] = acc;
+}
+
+__global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+    float acc = 0.0f;
+    for (int k = -R; k <= R; ++k) {
+        const int yy = y + k;
+        const float v = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
+        acc = __fmaf_rn(v, c.w[R - k], acc);
+    }
+    out[(size_t)y * n + x] = acc;
+}
+
+// optimized: the CTA's rows plus the apron staged once in shared memory
+__global__ void k_conv_rows_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
+    extern __shared__ float s[];  // [wy][wx + 2R]
+    const int wx = blockDim.x, wy = blockDim.y, P = wx + 2 * R;
+    const int x0 = blockIdx.x * wx - R, y = blockIdx.y * wy + threadIdx.y;
+    for (int t = threadIdx.x; t < P; t += wx) {
+        const int xx = x0 + t;
+        s[threadIdx.y * P + t] = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
+    }
+    __syncthreads();
+    float acc = 0.0f;
+    for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[threadIdx.y * P + threadIdx.x + R + k], c.w[R - k], acc);
+    out[(size_t)y * n + blockIdx.x * wx + threadIdx.x] = acc;
+}
+
+__global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
+    extern __shared__ float s[];  // [wy + 2R][wx]
+    const int wx = blockDim.x, wy = blockDim.y, H = wy + 2 * R;
+    const int x = blockIdx.x * wx + threadIdx.x, y0 = blockIdx.y * wy - R;
+    for (int t = threadIdx.y; t < H; t += wy) {
+        const int yy = y0 + t;
+        s[t * wx + threadIdx.x] = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
+    }
+    __syncthreads();
+    float acc = 0.0f;
+    for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[(threadIdx.y + R + k) * wx + threadIdx.x], c.w[R - k], acc);
+    out[(size_t)(blockIdx.y * wy + threadIdx.y) * n + x] = acc;
+}
+
+// ------------------------------------------------------------ MVT (Polybench)
+// x1[i] = x1_0[i] + sum_j A[i][j] * y1[j];  x2[i] = x2_0[i] + sum_j A[j][i] * y2[j]  (j ascending)
+__global__ void k_mvt1_base(const float *__restrict__ A, const float *__restrict__ y1, const float *__restrict__ x1_0,
+                            float *__restrict__ x1, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc = x1_0[i];
+    for (int j = 0; j < n; ++j) acc = __fmaf_rn(A[(size_t)i * n + j], y1[j], acc);  // row walk per thread
+    x1[i] = acc;
+}
+
+__global__ void k_mvt2_base(const float *__restrict__ A, const float *__restrict__ y2, const float *__restrict__ x2_0,
+                            float *__restrict__ x2, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc = x2_0[i];
+    for (int j = 0; j < n; ++j) acc = __fmaf_rn(A[(size_t)j * n + i], y2[j], acc);  // coalesced across threads
+    x2[i] = acc;
+}
+
+// optimized kernel 1: a [wg][T] tile of A (loaded along rows: coalesced) and
+// T entries of y1 staged per step
+__global__ void k_mvt1_opt(const float *__restrict__ A, const float *__restrict__ y1, const float *__restrict__ x1_0,
+                           float *__restrict__ x1, int n, int T) {
+    extern __shared__ float s[];  // sA[wg][T + 1], sy[T]
+    const int wg = blockDim.x, P = T + 1;
+    float *sA = s, *sy = s + wg * P;
+    const int i0 = blockIdx.x * wg, ti = threadIdx.x;
+    float acc = x1_0[i0 + ti];
+    for (int j0 = 0; j0 < n; j0 += T) {
+        for (int e = ti; e < wg * T; e += wg) {
+            const int r = e / T, cc = e - r * T;
+            sA[r * P + cc] = A[(size_t)(i0 + r) * n + j0 + cc];
+        }
+        for (int e = ti; e < T; e += wg) sy[e] = y1[j0 + e];
+        __syncthreads();
+        for (int jj = 0; jj < T; ++jj) acc = __fmaf_rn(sA[ti * P + jj], sy[jj], acc);
+        __syncthreads();
+    }
+    x1[i0 + ti] = acc;
+}
+
+// optimized kernel 2: A is already read coalesced; T entries of y2 staged per step
+__global__ void k_mvt2_opt(const float *__restrict__ A, const float *__restrict__ y2, const float *__restrict__ x2_0,
+                           float *__restrict__ x2, int n, int T) {
+    extern __shared__ float sy[];  // [T]
+    const int wg = blockDim.x;
+    const int i = blockIdx.x * wg + threadIdx.x;
+    float acc = x2_0[i];
+    for (int j0 = 0; j0 < n; j0 += T) {
+        for (int e = threadIdx.x; e < T; e += wg) sy[e] = y2[j0 + e];
+        __syncthreads();
+        for (int jj = 0; jj < T; ++jj) acc = __fmaf_rn(A[(size_t)(j0 + jj) * n + i], sy[jj], acc);
+        __syncthreads();
+    }
+    x2[i] = acc;
+}
+
+}  // namespace lmt
