@@ -54,7 +54,7 @@ def test_oracle_against_float64(kernel, radius):
 def test_instance_set_is_valid():
     insts = R.instance_set()
     assert {i.kernel for i in insts} == {0, 1, 2, 3}
-    assert len(insts) == 15 + 14 + 24 + 10
+    assert len(insts) == 15 + 14 + 24 + 10 + 6
     for i in insts:
         assert R.validate(i) == "", i
     assert R.validate(R.RealInstance(0, 2048, 16, 3, tile=16)) != ""
@@ -67,8 +67,9 @@ def test_gpu_matches_oracle_bitwise():
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    small = [R.RealInstance(i.kernel, {0: 128, 1: 128, 2: 128, 3: 256}[i.kernel], i.wg_x, i.wg_y, i.tile, i.radius)
-             for i in R.instance_set()]
+    small = [R.RealInstance(i.kernel, {0: 128, 1: 128, 2: 128, 3: 1024}[i.kernel], i.wg_x, i.wg_y, i.tile, i.radius)
+             for i in R.instance_set() if i.n <= 4096]
+    small = [i for i in small if R.validate(i) == ""]
     seen = set()
     for inst in small:
         key = (inst.kernel, inst.n, inst.radius)
