@@ -19,7 +19,17 @@ from .access_analysis import (
     kernel_time,
     label_speedup,
 )
-from .dataset import BuildResult, LabeledInstance, build_arrays, build_dataset, split_rows
+from .dataset import (
+    CSV_HEADER,
+    BuildResult,
+    LabeledInstance,
+    build_arrays,
+    build_dataset,
+    read_rows,
+    split_rows,
+    write_rows,
+    write_skip_log,
+)
 from .device import DEFAULT_DEVICE, DeviceDescriptor
 from .errors import (
     ConfigError,

@@ -229,3 +229,27 @@ def test_config4_forest_on_gpu_features_matches_reference():
     assert np.array_equal(pred[::8], ev["pred_every8"])
     assert hashlib.sha256(pred.tobytes()).digest() == ev["pred_sha256"].tobytes()
     assert np.array_equal(fb.label[::8], ev["speedup_every8"])
+
+
+def test_run_sweep_checkpoint_resume_and_dataset(tmp_path):
+    """The sweep job on one GPU: chunks checkpointed, a second run resumes
+    every chunk, labels + the 39-column dataset written (rows = the K4 rows
+    of this rank's share)."""
+    import json
+
+    from paper_1412_6986_b200 import run_sweep
+
+    out = str(tmp_path / "sweep")
+    argv = ["--out", out, "--max-instances", "3000", "--seed", "2", "--chunk", "8", "--limit", "24"]
+    s1 = run_sweep.run(argv)
+    assert s1["rows"] == 24 and s1["chunks_resumed"] == 0 and s1["mismatched"] == 0
+    s2 = run_sweep.run(argv)
+    assert s2["chunks_resumed"] == 3
+    lab = np.load(f"{out}/labels.npz")
+    assert len(lab["row"]) == 24 and (lab["t_base_ms"] > 0).all()
+    rows = L.read_rows(f"{out}/dataset.csv")
+    assert len(rows) == 24
+    table = L.select_instance_table(L.SamplingSpec(max_instances=3000, seed=2))
+    fb = L.features_records(table.records(lab["row"]))
+    assert np.array_equal(np.stack([r.features.to_array() for r in rows]), fb.X)
+    assert json.load(open(f"{out}/summary.json"))["total_rows"] == 24

@@ -177,3 +177,49 @@ def test_split_against_reference(lmtune_ref):
     rows = list(range(1234))
     for seed in (0, 1, 99):
         assert L.split_rows(rows, 0.1, seed) == ref_split(rows, 0.1, seed)
+
+
+def test_dataset_csv_matches_reference_bytes(lmtune_ref, tmp_path):
+    """write_rows is byte-identical to dataset.write_rows; read_rows parses the
+    reference's file back losslessly (dataset.py:284-404)."""
+    import numpy as np
+    from lmtune import dataset as ref_ds
+
+    import paper_1412_6986_b200 as L
+    from conftest import make_instance
+
+    res = ref_ds.build_dataset(ref_ds.SamplingSpec(max_instances=300, seed=4))
+    ref_path, our_path = tmp_path / "ref.csv", tmp_path / "ours.csv"
+    ref_ds.write_rows(ref_path, res.rows)
+    ours = []
+    for r in res.rows:
+        p, lc = r.instance.params, r.instance.launch
+        rec = dict(in_h=p.in_h, in_w=p.in_w, out_h=p.out_h, out_w=p.out_w, pattern=p.pattern.value, n=p.n, m=p.m,
+                   shape=p.stencil.shape.value, radius=p.stencil.radius, num_comp_ilb=p.num_comp_ilb,
+                   num_comp_ep=p.num_comp_ep, num_coal_ilb=p.num_coal_ilb, num_coal_ep=p.num_coal_ep,
+                   num_uncoal_ilb=p.num_uncoal_ilb, num_uncoal_ep=p.num_uncoal_ep, grid_x=lc.grid_x,
+                   grid_y=lc.grid_y, wg_x=lc.wg_x, wg_y=lc.wg_y)
+        ours.append(L.LabeledInstance(make_instance(rec), L.FeatureVector.from_array(r.features.to_array()),
+                                      r.speedup, r.beneficial))
+    L.write_rows(our_path, ours)
+    assert our_path.read_bytes() == ref_path.read_bytes()
+    back = L.read_rows(ref_path)
+    assert len(back) == len(res.rows)
+    for a, b in zip(back, res.rows):
+        assert np.array_equal(a.features.to_array(), b.features.to_array()) and a.speedup == b.speedup
+        assert L.sweep.instance_key(a.instance) == ref_ds.instance_key(b.instance)
+    assert L.CSV_HEADER == ref_ds.CSV_HEADER
+
+
+def test_dataset_csv_errors_name_the_line(tmp_path):
+    import pytest
+
+    import paper_1412_6986_b200 as L
+
+    p = tmp_path / "bad.csv"
+    p.write_text(",".join(L.CSV_HEADER) + "\nxy_reuse,rect,1\n")
+    with pytest.raises(L.DatasetFormatError, match="line 2"):
+        L.read_rows(p)
+    p.write_text("a,b\n")
+    with pytest.raises(L.DatasetFormatError, match="line 1"):
+        L.read_rows(p)
