@@ -1038,7 +1038,12 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
     std::sort(keys.begin(), keys.end());
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
     std::string err;
-    const int nt = nthreads > 0 ? nthreads : (int)std::max(1u, std::thread::hardware_concurrency());
+    int nt = nthreads;
+    if (nt <= 0) {  // all cores, shared among the processes of this node (one per GPU)
+        const char *lw = getenv("LOCAL_WORLD_SIZE");
+        const int procs = lw ? std::max(1, atoi(lw)) : 1;
+        nt = std::max(1, (int)std::thread::hardware_concurrency() / procs);
+    }
     int rc = g_jit.prepare(keys, nt, &err);
     if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
     for (const JitKey &k : keys) {  // load the modules now, not inside a timed batch
