@@ -154,15 +154,14 @@ __host__ __device__ constexpr int row_first(int dr) {
 // scalar loads -- the "coalesced, vectorised (128-bit) global loads" of the
 // baseline, fewer L1 wavefronts when the lanes of a warp walk different rows.
 struct GlobalSrc {
-    const float *p[U];  // element (home row, home col) of (i=0, j=0), per work unit
+    const float *p[U];  // element of the step being loaded next, per work unit
     int pitch;
     long long cs;       // floats between copies of `in`
     template <int NU_>
-    __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
-        const int step = r * pitch + c;
+    __device__ __forceinline__ void load(float (&v)[NU_][KT]) const {
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
-            const float *q = p[u] + step;
+            const float *q = p[u];
 #pragma unroll
             for (int dr = -RAD; dr <= RAD; ++dr) {
                 const int w = row_w(dr), k0 = row_first(dr), nt = 2 * w + 1;
@@ -179,11 +178,21 @@ struct GlobalSrc {
                         if (4 * b + 3 < nt) v[u][k0 + 4 * b + 3] = x.w;
                     }
                 } else {
+                    // the row pointer once, the taps as immediate offsets of it
+                    const float *rp = q + dr * pitch;
 #pragma unroll
-                    for (int t = 0; t < nt; ++t) v[u][k0 + t] = __ldg(q + (dr * pitch + t - w));
+                    for (int t = 0; t < nt; ++t) v[u][k0 + t] = __ldg(rp + (t - w));
                 }
             }
         }
+    }
+    // move every work unit's pointer by (dr, dc) home-coordinate steps: one
+    // 64-bit add per work unit (the offset is uniform)
+    template <int NU_>
+    __device__ __forceinline__ void step(int dr, int dc) {
+        const long long d = (long long)dr * pitch + dc;
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) p[u] += d;
     }
 };
 
@@ -191,31 +200,50 @@ struct GlobalSrc {
 struct SmemSrc {
     const float *p[U];  // shared-memory element of (i=0, j=0), per work unit
     int pitch;
+    int r = 0, c = 0;   // home-coordinate offset of the step being loaded next
     template <int NU_>
-    __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
+    __device__ __forceinline__ void load(float (&v)[NU_][KT]) const {
+        const int off = r * pitch + c;  // 32-bit shared addresses: recomputing is cheaper than more live pointers
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
-            const float *q = p[u] + (r * pitch + c);
+            const float *q = p[u] + off;
 #pragma unroll
-            for (int k = 0; k < KT; ++k) v[u][k] = q[tap_dr(k) * pitch + tap_dc(k)];
+            for (int dr = -RAD; dr <= RAD; ++dr) {
+                const float *rp = q + dr * pitch;
+#pragma unroll
+                for (int t = 0; t < 2 * row_w(dr) + 1; ++t) v[u][row_first(dr) + t] = rp[t - row_w(dr)];
+            }
         }
+    }
+    template <int NU_>
+    __device__ __forceinline__ void step(int dr, int dc) {
+        r += dr;
+        c += dc;
     }
 };
 
 // K2 with several 256-wide column chunks: smem [ccol][rows_padded][256].
 struct SmemWideSrc {
     const float *slot[U];  // stage base per work unit
-    int hr[U], hc[U];      // region coordinate of (i=0, j=0) per work unit
+    int hr[U], hc[U];      // region coordinate of the step being loaded next, per work unit
     int chunk;             // rows_padded * 256
     template <int NU_>
-    __device__ __forceinline__ void load(float (&v)[NU_][KT], int r, int c) const {
+    __device__ __forceinline__ void load(float (&v)[NU_][KT]) const {
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
 #pragma unroll
             for (int k = 0; k < KT; ++k) {
-                const int row = hr[u] + r + tap_dr(k), col = hc[u] + c + tap_dc(k);
+                const int row = hr[u] + tap_dr(k), col = hc[u] + tap_dc(k);
                 v[u][k] = slot[u][(col >> 8) * chunk + row * 256 + (col & 255)];
             }
+        }
+    }
+    template <int NU_>
+    __device__ __forceinline__ void step(int dr, int dc) {
+#pragma unroll
+        for (int u = 0; u < NU_; ++u) {
+            hr[u] += dr;
+            hc[u] += dc;
         }
     }
 };
@@ -234,7 +262,6 @@ struct Slot {
 
 // Load cursor: the (i, j) step a slot is filled for.
 struct Cursor {
-    int r, c;          // home-coordinate offset of the step from (i=0, j=0)
     int j;
     const float *crow; // coal: in2 row trow at column glin % IN2_W
     int trow;
@@ -289,7 +316,7 @@ __device__ __forceinline__ void fill(Slot<NU_> &s, const Src &src, const Cursor 
     // the one new coal row a step touches (rows trow .. trow+NC-1), PF steps ahead
     if (NC > 0) prefetch_l1(q.crow + (NC - 1 + PF) * P2);
 #endif
-    src.template load<NU_>(s.v, q.r, q.c);
+    src.template load<NU_>(s.v);
 #pragma unroll
     for (int k = 0; k < NC; ++k) s.c[k] = ctx_coal(A, in2c, q.crow, q.trow, k);
 #if LMT_CTXWRAP
@@ -300,15 +327,17 @@ __device__ __forceinline__ void fill(Slot<NU_> &s, const Src &src, const Cursor 
 #endif
 }
 
-__device__ __forceinline__ void advance(Cursor &q, const SynthArgs &A, const float *in2c, const float *in2u) {
+template <int NU_, class Src>
+__device__ __forceinline__ void advance(Cursor &q, Src &src, const SynthArgs &A, const float *in2c,
+                                        const float *in2u) {
     // j-walk, then the i carriage return (home coordinate affine in i, j)
-    q.r += A.a[3];
-    q.c += A.a[7];
+    int dr = A.a[3], dc = A.a[7];
     if (++q.j == A.M) {
         q.j = 0;
-        q.r += A.a[2] - A.M * A.a[3];
-        q.c += A.a[6] - A.M * A.a[7];
+        dr += A.a[2] - A.M * A.a[3];
+        dc += A.a[6] - A.M * A.a[7];
     }
+    src.template step<NU_>(dr, dc);
     // (i*M + j) mod IN2_H / IN2_W
     if (++q.trow == H2) {
         q.trow = 0;
@@ -346,18 +375,18 @@ __device__ __forceinline__ void consume(float (&acc)[NU_], const Slot<NU_> &s) {
 
 // NU_ work units of one thread: the full i/j nest then the epilogue.
 template <int NU_, class Src>
-__device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, const float *in2c, const float *in2u,
+__device__ __forceinline__ void run_units(const SynthArgs &A, Src src, const float *in2c, const float *in2u,
                                           float (&acc)[NU_]) {
 #pragma unroll
     for (int u = 0; u < NU_; ++u) acc[u] = 0.0f;
     const int NM = A.N * A.M;
-    Cursor q{0, 0, 0, in2c, 0, in2u, 0};
+    Cursor q{0, in2c, 0, in2u, 0};
     Slot<NU_> s[D];
 #pragma unroll
     for (int d = 0; d < D - 1; ++d)
         if (d < NM) {
             fill<NU_>(s[d], src, q, A, in2c, in2u);
-            advance(q, A, in2c, in2u);
+            advance<NU_>(q, src, A, in2c, in2u);
         }
     int t0 = 0;
     // steady state: whole blocks of D steps whose prefetches are all in range,
@@ -367,7 +396,7 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, co
 #pragma unroll
         for (int d = 0; d < D; ++d) {
             fill<NU_>(s[(d + D - 1) % D], src, q, A, in2c, in2u);
-            advance(q, A, in2c, in2u);
+            advance<NU_>(q, src, A, in2c, in2u);
             consume<NU_>(acc, s[d]);
         }
     }
@@ -378,7 +407,7 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, const Src &src, co
             if (t < NM) {
                 if (t + D - 1 < NM) {
                     fill<NU_>(s[(d + D - 1) % D], src, q, A, in2c, in2u);
-                    advance(q, A, in2c, in2u);
+                    advance<NU_>(q, src, A, in2c, in2u);
                 }
                 consume<NU_>(acc, s[d]);
             }

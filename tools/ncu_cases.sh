@@ -14,8 +14,10 @@ B=2048,2048,2048,2048,0,16,16,2,1,6,44,13,0,2,4,256,2048,2,1
 C=1024,1024,1024,1024,5,1,1,2,1,0,0,0,0,0,0,1024,1024,16,16
 D=2048,2048,2048,2048,1,64,2,0,1,17,24,8,12,4,0,16,128,8,128
 E=2048,2048,1024,1024,0,64,64,1,0,26,38,10,13,2,2,4,256,1,256
+I=2048,2048,2048,2048,0,32,16,0,1,35,19,6,13,4,4,128,4,64,2
+K=2048,2048,1024,1024,0,32,32,1,1,33,28,10,2,3,2,4,128,1,64
 CASES=${CASES:-A B C D E}
-python tools/ncu_one.py $A $B $C $D $E > $OUT/times.txt 2>&1
+python tools/ncu_one.py $A $B $C $D $E $I $K > $OUT/times.txt 2>&1
 for c in $CASES; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_synth|lmt_kernel" -c 2 \
      -o $OUT/prof_$c python tools/ncu_one.py ${!c} > $OUT/ncu_$c.log 2>&1
