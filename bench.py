@@ -69,8 +69,23 @@ def step_rows(perm, step: int, world: int, batch: int):
     return g
 
 
-def shard_for_rank(L, table, rows, world: int, rank: int):
-    return L.dist.rank_rows(table, rows, world, rank)
+_SHARES = {}
+
+
+def shard_for_rank(L, table, perm, step: int, world: int, rank: int, batch: int):
+    """This rank's share of step `step`'s global batch. Steps are assigned in
+    order with the predicted per-rank load carried over (longest-processing-
+    time on the launch-floor cost), identically on every rank, so the ranks
+    stay balanced over the whole run; memoised so every pass over a step
+    (compile, warm-up, timed, e2e) sees the same share."""
+    key = (world, rank, batch)
+    if key not in _SHARES:
+        _SHARES[key] = ([], np.zeros(world))
+    shares, loads = _SHARES[key]
+    while len(shares) <= step:
+        s = len(shares)
+        shares.append(L.dist.rank_rows(table, step_rows(perm, s, world, batch), world, rank, loads))
+    return shares[step]
 
 
 # ------------------------------------------------------------------ clocks
@@ -219,14 +234,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # compile + load every specialised kernel the run will launch (NVRTC,
     # sm_100a; the reference's per-kernel compile step), before any timing
     t_prep = time.perf_counter()
-    all_rows = np.concatenate([shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+    all_rows = np.concatenate([shard_for_rank(L, table, perm, s, world, rank, args.batch)
                                for s in range(args.warmup + args.steps)])
     n_kernels = L.prepare_records(table.records(all_rows))
     t_prep = time.perf_counter() - t_prep
     jit_compiled, jit_seconds = _lib.jit_stats()
 
     for s in range(args.warmup):
-        rows = shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+        rows = shard_for_rank(L, table, perm, s, world, rank, args.batch)
         L.measure_records(table.records(rows))
 
     # ---- timed region: device-resident inputs (generated by K0 inside the step)
@@ -237,7 +252,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     with ClockSampler(local_rank) as clocks:
         ev0.record(lib_stream)
         for s in range(args.warmup, args.warmup + args.steps):
-            rows = shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+            rows = shard_for_rank(L, table, perm, s, world, rank, args.batch)
             res = L.measure_records(table.records(rows))
             results.append((rows, res))
         ev1.record(lib_stream)
@@ -469,7 +484,7 @@ def run_e2e(args, L, table, perm, world, rank, barrier):
     in2_host = None
     pinned_bytes = 0
     for s in steps:
-        rows = shard_for_rank(L, table, step_rows(perm, s, world, args.batch), world, rank)
+        rows = shard_for_rank(L, table, perm, s, world, rank, args.batch)
         insts = table.instances(rows)
         keep = []
         for inst in insts:

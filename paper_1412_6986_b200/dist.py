@@ -17,14 +17,16 @@ from . import sweep
 LABEL_COLUMNS = ("row", "t_base_ms", "t_opt_ms")
 
 
-def rank_rows(table, rows: np.ndarray, world: int, rank: int) -> np.ndarray:
+def rank_rows(table, rows: np.ndarray, world: int, rank: int, loads: np.ndarray | None = None) -> np.ndarray:
     """This rank's share of `rows` (greedy longest-processing-time on the
-    estimated cost; shares are disjoint and cover `rows`)."""
+    launch-floor cost, sweep.launch_cost; shares are disjoint and cover
+    `rows`). Pass the same `loads` array (length world) for consecutive
+    batches on every rank to balance across batches too."""
     rows = np.asarray(rows)
     if world == 1:
         return rows
-    cost = sweep.estimated_cost(table.records(rows))
-    return rows[sweep.shard_balanced(cost, world)[rank]]
+    cost = sweep.launch_cost(table.records(rows))
+    return rows[sweep.shard_balanced(cost, world, loads)[rank]]
 
 
 def label_matrix(rows: np.ndarray, res: np.ndarray) -> np.ndarray:
