@@ -446,6 +446,17 @@ def run_rf(args, L, world, rank, barrier):
     t0 = time.perf_counter()
     pred = L.predict(forest, fb.X)  # host X in, host predictions out (2 ** mean in numpy)
     t_e2e = time.perf_counter() - t0
+    train_info = {}
+    if rank == 0:  # the native trainer on the GPU-featurised 10% (forest.train, bit-exact)
+        tr = L.features_records(table.records(ev["train_idx"]))
+        y = np.array([L.speedup_to_target(v) for v in tr.label])
+        t0 = time.perf_counter()
+        trained = L.train_arrays(tr.X, y, L.Hyperparams(num_trees=20, features_per_node=4, seed=0),
+                                 threads=min(20, os.cpu_count() or 1))
+        train_info = {"train_s": time.perf_counter() - t0, "train_rows": int(len(y)),
+                      "trained_forest_bitwise_reference": all(
+                          np.array_equal(a.threshold, b.threshold) and np.array_equal(a.value, b.value)
+                          and np.array_equal(a.feature, b.feature) for a, b in zip(forest.trees, trained.trees))}
     t = torch.tensor([t_feat, t_k3, t_e2e], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -454,7 +465,8 @@ def run_rf(args, L, world, rank, barrier):
                        "SamplingSpec(100k, seed=0)), held-out 90% = 90,000 rows",
            "trees": len(forest.trees), "nodes": int(sum(len(tr.feature) for tr in forest.trees)),
            "rows": int(len(held)), "k3_rows_per_s": len(held) / t_k3,
-           "predict_e2e_rows_per_s": len(held) / t_e2e, "k4_features_rows_per_s": len(held) / t_feat}
+           "predict_e2e_rows_per_s": len(held) / t_e2e, "k4_features_rows_per_s": len(held) / t_feat,
+           **train_info}
     if world == 1:
         out["features_bitwise_reference"] = hashlib.sha256(fb.X.tobytes()).digest() == ev["X_sha256"].tobytes()
         out["predictions_bitwise_reference"] = bool(

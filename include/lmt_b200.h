@@ -205,6 +205,18 @@ int lmt_real_execute(const lmt_real_instance *inst, int variant, const float *co
  * and compared bitwise on the device (same record as lmt_measure_batch). */
 int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, lmt_measurement *out);
 
+/* Random-forest training, one tree (forest.py:72-163 _best_split /
+ * _build_tree), on the host, bit-identical to the reference. The random
+ * draws are numpy's, generated by the caller from the tree's PCG64 stream in
+ * the reference's order: `sample` = the bootstrap rows (or 0..n-1), `draws`
+ * = ndraws x k sorted feature subsets, one per split attempt in DFS order.
+ * Outputs the node arrays (capacity `cap`, >= 2*nsample - 1 suffices).
+ * LMT_ERR_TOO_LARGE with *draws_used = -1: call again with more draws. */
+int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t nfeat, const int64_t *sample,
+                      int64_t nsample, const int32_t *draws, int64_t ndraws, int32_t k, int32_t max_depth,
+                      int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left,
+                      int32_t *right, double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used);
+
 /* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
  * compiles) and the host seconds spent compiling. */
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);

@@ -39,7 +39,19 @@ from .errors import (
     ModelFormatError,
     OptimizationInfeasible,
 )
-from .forest import Forest, GpuForest, Hyperparams, Tree, decide, load, predict, save, speedup_to_target
+from .forest import (
+    Forest,
+    GpuForest,
+    Hyperparams,
+    Tree,
+    decide,
+    load,
+    predict,
+    save,
+    speedup_to_target,
+    train,
+    train_arrays,
+)
 from .geometry import (
     AffineAccess,
     EmitGeometry,

@@ -21,6 +21,7 @@
 #include "lmt_jit_host.cuh"
 #include "lmt_features.cuh"
 #include "lmt_real.cuh"
+#include "lmt_train.h"
 
 #ifndef LMT_VERSION
 #define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
@@ -1362,6 +1363,32 @@ int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, l
         }
     }
     for (auto &e : ev) cudaEventDestroy(e);
+    return LMT_OK;
+}
+
+int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t nfeat, const int64_t *sample,
+                      int64_t nsample, const int32_t *draws, int64_t ndraws, int32_t k, int32_t max_depth,
+                      int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left, int32_t *right,
+                      double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used) {
+    if (!X || !y || !sample || nsample < 1 || nfeat < 1 || k < 1 || (!draws && ndraws > 0) || !nodes_out ||
+        !draws_used)
+        return fail(LMT_ERR_ARG, "bad train arguments");
+    for (int64_t i = 0; i < nsample; i++)
+        if (sample[i] < 0 || sample[i] >= nrows) return fail(LMT_ERR_ARG, "sample row out of range");
+    TreeOut t;
+    if (build_tree(X, y, nfeat, sample, nsample, draws, ndraws, k, max_depth, min_samples_leaf, &t)) {
+        *draws_used = -1;
+        return fail(LMT_ERR_TOO_LARGE, "tree needs more than %lld feature draws", (long long)ndraws);
+    }
+    const int64_t nn = (int64_t)t.feature.size();
+    *nodes_out = nn;
+    *draws_used = t.draws_used;
+    if (nn > cap) return fail(LMT_ERR_TOO_LARGE, "tree has %lld nodes > capacity %lld", (long long)nn, (long long)cap);
+    std::copy(t.feature.begin(), t.feature.end(), feature);
+    std::copy(t.threshold.begin(), t.threshold.end(), threshold);
+    std::copy(t.left.begin(), t.left.end(), left);
+    std::copy(t.right.begin(), t.right.end(), right);
+    std::copy(t.value.begin(), t.value.end(), value);
     return LMT_OK;
 }
 

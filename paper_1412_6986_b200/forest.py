@@ -74,6 +74,85 @@ class Forest:
     trees: list[Tree] = field(default_factory=list)
 
 
+def _tree_draws(seed: int, n: int, nfeat: int, hp: Hyperparams, ndraws: int):
+    """The tree's numpy draws in the reference's order (forest.py:117-122, 77):
+    bootstrap rows, then one sorted feature subset per split attempt."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    if hp.bootstrap:
+        sample = rng.integers(0, n, size=n)
+        oob = np.setdiff1d(np.arange(n), sample)
+    else:
+        sample = np.arange(n)
+        oob = None
+    k = min(hp.features_per_node, nfeat)
+    draws = np.empty((ndraws, k), dtype=np.int32)
+    for i in range(ndraws):
+        draws[i] = np.sort(rng.choice(nfeat, size=k, replace=False))
+    return np.ascontiguousarray(sample, dtype=np.int64), oob, draws
+
+
+def _build_tree(X: np.ndarray, y: np.ndarray, hp: Hyperparams, tree_seed: int) -> Tree:
+    """forest.py:117-163 in native code (lmt_rf_train_tree), bit-identical."""
+    n, nfeat = X.shape
+    ndraws = min(2 * n, 4096)
+    while True:
+        sample, oob, draws = _tree_draws(tree_seed, n, nfeat, hp, ndraws)
+        cap = 2 * n + 1
+        feat = np.empty(cap, dtype=np.int32)
+        thr = np.empty(cap, dtype=np.float64)
+        left = np.empty(cap, dtype=np.int32)
+        right = np.empty(cap, dtype=np.int32)
+        val = np.empty(cap, dtype=np.float64)
+        nodes, used = ctypes.c_int64(), ctypes.c_int64()
+        vp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        rc = lib().lmt_rf_train_tree(vp(X), vp(y), n, nfeat, vp(sample), len(sample), vp(draws), len(draws),
+                                     draws.shape[1], -1 if hp.max_depth is None else hp.max_depth,
+                                     hp.min_samples_leaf, vp(feat), vp(thr), vp(left), vp(right), vp(val), cap,
+                                     ctypes.byref(nodes), ctypes.byref(used))
+        if rc != 0 and used.value == -1 and ndraws < 2 * n + 1:
+            ndraws = min(2 * n + 1, ndraws * 4)  # more split attempts than drawn: draw more
+            continue
+        check(rc, what="rf_train_tree")
+        m = nodes.value
+        return Tree(feat[:m].copy(), thr[:m].copy(), left[:m].copy(), right[:m].copy(), val[:m].copy(),
+                    oob_indices=oob)
+
+
+def train_arrays(X, y, hp: Hyperparams, feature_names=None, threads: int = 1) -> Forest:
+    """forest.train_arrays (forest.py:166-188): fit on a feature matrix and
+    log2-speedup targets; trees built natively, in parallel host threads,
+    results independent of the thread count."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .seeding import mix_seed
+
+    X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
+    if X.ndim != 2 or len(X) != len(y):
+        raise ValueError(f"bad training shapes {X.shape} vs {y.shape}")
+    if len(y) == 0:
+        raise ValueError("empty training set")
+    if feature_names is None:
+        feature_names = tuple(f"f{i}" for i in range(X.shape[1]))
+    seeds = [mix_seed(hp.seed, t) for t in range(hp.num_trees)]
+    if threads > 1:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            trees = list(pool.map(lambda s: _build_tree(X, y, hp, s), seeds))
+    else:
+        trees = [_build_tree(X, y, hp, s) for s in seeds]
+    return Forest(hyperparams=hp, feature_names=tuple(feature_names), trees=trees)
+
+
+def train(rows, hp: Hyperparams = Hyperparams(), threads: int = 1) -> Forest:
+    """forest.train (forest.py:191-196): rows with .features and .speedup;
+    target log2(speedup), infeasible floored at -10."""
+    from .access_analysis import FEATURE_NAMES
+
+    X = np.stack([r.features.to_array() for r in rows])
+    y = np.array([speedup_to_target(r.speedup) for r in rows], dtype=np.float64)
+    return train_arrays(X, y, hp, feature_names=FEATURE_NAMES, threads=threads)
+
+
 def speedup_to_target(speedup: float) -> float:
     """log2 target with the infeasible floor (forest.py:68-69)."""
     return math.log2(speedup) if speedup > 0 else TARGET_FLOOR

@@ -229,6 +229,13 @@ def test_config4_forest_on_gpu_features_matches_reference():
     assert np.array_equal(pred[::8], ev["pred_every8"])
     assert hashlib.sha256(pred.tobytes()).digest() == ev["pred_sha256"].tobytes()
     assert np.array_equal(fb.label[::8], ev["speedup_every8"])
+    # and the forest itself, trained natively on the GPU-featurised 10%
+    tr = L.features_records(table.records(ev["train_idx"]))
+    y = np.array([L.speedup_to_target(s) for s in tr.label])
+    ours = L.train_arrays(tr.X, y, L.Hyperparams(num_trees=20, features_per_node=4, seed=0), threads=8)
+    for a, b in zip(f.trees, ours.trees):
+        assert np.array_equal(a.feature, b.feature) and np.array_equal(a.threshold, b.threshold)
+        assert np.array_equal(a.value, b.value)
 
 
 def test_run_sweep_checkpoint_resume_and_dataset(tmp_path):

@@ -223,3 +223,33 @@ def test_dataset_csv_errors_name_the_line(tmp_path):
     p.write_text("a,b\n")
     with pytest.raises(L.DatasetFormatError, match="line 1"):
         L.read_rows(p)
+
+
+def test_train_matches_reference(lmtune_ref, tmp_path):
+    """forest.train (forest.py:72-196): the native tree builder gives the
+    reference's trees node for node and a byte-identical model file."""
+    import numpy as np
+    from lmtune import forest as ref_forest
+
+    import paper_1412_6986_b200 as L
+    from conftest import GOLDEN_DIR
+
+    ev = np.load(f"{GOLDEN_DIR}/forest_eval.npz")
+    X = ev["X"][:900]
+    y = np.array([L.speedup_to_target(s) for s in ev["speedup"][:900]])
+    for hp_args in (dict(num_trees=4, features_per_node=4, seed=3),
+                    dict(num_trees=3, features_per_node=6, seed=1, max_depth=7, min_samples_leaf=3),
+                    dict(num_trees=2, features_per_node=18, seed=9, bootstrap=False)):
+        ref = ref_forest.train_arrays(X, y, ref_forest.Hyperparams(**hp_args))
+        ours = L.train_arrays(X, y, L.Hyperparams(**hp_args), threads=2)
+        assert len(ref.trees) == len(ours.trees)
+        for a, b in zip(ref.trees, ours.trees):
+            for f in ("feature", "threshold", "left", "right", "value"):
+                assert np.array_equal(getattr(a, f), getattr(b, f)), f
+            if a.oob_indices is None:
+                assert b.oob_indices is None
+            else:
+                assert np.array_equal(a.oob_indices, b.oob_indices)
+        ref_forest.save(ref, tmp_path / "r.txt")
+        L.save(ours, tmp_path / "o.txt")
+        assert (tmp_path / "r.txt").read_bytes() == (tmp_path / "o.txt").read_bytes()
