@@ -217,6 +217,13 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
                       int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left,
                       int32_t *right, double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used);
 
+/* The CUDA source the specialised kernel of (instance, variant) is compiled
+ * from -- its #defines then the kernel text -- the counterpart of
+ * codegen.emit_baseline / emit_optimized (codegen.py:336-354). *len_out =
+ * bytes needed (without the NUL); buf may be NULL to query. */
+int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, char *buf, int64_t cap,
+                      int64_t *len_out);
+
 /* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
  * compiles) and the host seconds spent compiling. */
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);

@@ -9,16 +9,21 @@ liblmt_b200.so (hand-written sm_100a CUDA behind a C ABI, include/lmt_b200.h);
 there is no CPU fallback.
 """
 
-from . import access_analysis, dataset, dist, measure, real, sweep  # noqa: F401
+from . import access_analysis, codegen, cost_model, dataset, dist, measure, metrics, real, sweep  # noqa: F401
 from .access_analysis import (
     FEATURE_NAMES,
     FeatureVector,
     TimeEstimate,
+    coalescing_degree,
     extract_features,
     features_records,
     kernel_time,
     label_speedup,
+    reuse_degree,
 )
+from .codegen import KernelSource, defines_manifest, emit_baseline, emit_optimized, kernel_filename
+from .cost_model import ResourceUsage, estimate_registers, occupancy, resource_usage
+from .metrics import EvalReport, count_accuracy, evaluate, penalty_weighted_accuracy, speedup_histogram
 from .dataset import (
     CSV_HEADER,
     BuildResult,

@@ -83,7 +83,7 @@ EXPORTS = (
     "lmt_execute", "lmt_measure_batch", "lmt_measure_batch_host", "lmt_digest",
     "lmt_rf_create", "lmt_rf_mean", "lmt_rf_mean_host", "lmt_rf_destroy", "lmt_sync",
     "lmt_get_stream", "lmt_prepare", "lmt_jit_stats", "lmt_features", "lmt_real_validate",
-    "lmt_real_execute", "lmt_real_measure", "lmt_rf_train_tree",
+    "lmt_real_execute", "lmt_real_measure", "lmt_rf_train_tree", "lmt_kernel_source",
 )
 
 _lib = None
@@ -121,6 +121,7 @@ def _declare(L):
     L.lmt_real_measure.argtypes = [P(CRealInstance), c_i64, c_i32, P(CMeasurement)]
     L.lmt_rf_train_tree.argtypes = [vp, vp, c_i64, c_i32, vp, c_i64, vp, c_i64, c_i32, c_i32, c_i32, vp, vp, vp,
                                     vp, vp, c_i64, P(c_i64), P(c_i64)]
+    L.lmt_kernel_source.argtypes = [P(CInstance), P(CDevice), ctypes.c_int, ctypes.c_char_p, c_i64, P(c_i64)]
     L.lmt_features.argtypes = [P(CInstance), c_i64, P(CDevice), c_i64, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         fn = getattr(L, name)

@@ -1392,6 +1392,30 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
     return LMT_OK;
 }
 
+int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, char *buf, int64_t cap,
+                      int64_t *len_out) {
+    if (!inst || (variant != 0 && variant != 1)) return fail(LMT_ERR_ARG, "bad kernel_source arguments");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c = nullptr;
+    lmt_geometry g0;
+    const lmt_device d = dev_or_default(dev);
+    int rc = compute_geometry(*inst, d, &g0);
+    if (rc) return rc;
+    Plan pl;
+    if (!violations(*inst).empty()) {
+        std::string m;
+        for (auto &v : violations(*inst)) m += (m.empty() ? "" : "; ") + v;
+        return fail(LMT_ERR_INVALID_INSTANCE, "%s", m.c_str());
+    }
+    rc = make_plan(*inst, d, round_up(g0.alloc_w, 4), &pl, c);
+    if (rc) return rc;
+    if (!pl.jit) return fail(LMT_ERR_ARG, "specialised kernels disabled (LMT_JIT=0)");
+    const std::string src = (variant == 0 ? pl.kb : pl.ko).defines() + kLmtJitSource;
+    if (len_out) *len_out = (int64_t)src.size();
+    if (buf && cap > 0) snprintf(buf, (size_t)cap, "%s", src.c_str());
+    return LMT_OK;
+}
+
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds) {
     if (kernels_compiled) *kernels_compiled = g_jit.compiled();
     if (compile_seconds) *compile_seconds = g_jit.compile_seconds();
