@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import paper_1412_6986_b200 as L
-from conftest import REF_SRC, make_instance
+from conftest import make_instance
 
 
 def test_every_reference_export_exists(lmtune_ref):
@@ -88,4 +88,3 @@ def test_emit_optimized_infeasible(golden):
                          5, 1, 0, 0, 0, 0)
     with pytest.raises(L.OptimizationInfeasible):
         L.emit_optimized(L.KernelInstance(p, L.LaunchConfig(2048, 2048, 32, 32)))
-    del REF_SRC
