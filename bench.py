@@ -453,10 +453,16 @@ def run_rf(args, L, world, rank, barrier):
         t0 = time.perf_counter()
         trained = L.train_arrays(tr.X, y, L.Hyperparams(num_trees=20, features_per_node=4, seed=0),
                                  threads=min(20, os.cpu_count() or 1))
-        train_info = {"train_s": time.perf_counter() - t0, "train_rows": int(len(y)),
-                      "trained_forest_bitwise_reference": all(
-                          np.array_equal(a.threshold, b.threshold) and np.array_equal(a.value, b.value)
-                          and np.array_equal(a.feature, b.feature) for a, b in zip(forest.trees, trained.trees))}
+        t_train = time.perf_counter() - t0
+        trained = L.Forest(trained.hyperparams, forest.feature_names, trained.trees)
+        with tempfile.NamedTemporaryFile(suffix=".txt", delete=False) as tmpf:
+            pass
+        L.save(trained, tmpf.name)
+        with gzip.open(os.path.join(gdir, "forest_sweep100k.txt.gz"), "rb") as fh:
+            same = open(tmpf.name, "rb").read() == fh.read()
+        os.unlink(tmpf.name)
+        train_info = {"train_s": t_train, "train_rows": int(len(y)), "train_threads": min(20, os.cpu_count() or 1),
+                      "trained_model_file_bitwise_reference": same}
     t = torch.tensor([t_feat, t_k3, t_e2e], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
