@@ -382,10 +382,28 @@ double in_union(const lmt_instance &p) {
 constexpr int kMaxStagesJ = 16;
 JitCache g_jit;
 
+// kernel_id of a specialised pair: 1 B D O E with B/O = log2 U + 1 of the
+// baseline/optimized kernel and D/E their prefetch depths (e.g. 14342:
+// baseline U=8 D=3, optimized U=8 D=2)
+int jit_kid(const JitKey &b, const JitKey &o) {
+    auto lg = [](int u) { int l = 0; while ((1 << l) < u) l++; return l + 1; };
+    return 10000 + lg(b.U) * 1000 + b.D * 100 + lg(o.U) * 10 + o.D;
+}
+
 int jit_pf() {
     const char *e = getenv("LMT_PF");
     const int v = e ? atoi(e) : 8;
     return std::max(0, std::min(v, kPfMax - 1));
+}
+
+// Largest work-units-per-thread candidate: 16 for the baseline (measured on
+// B200: 10-22 % faster than 8 on launches with one warp per SM
+// sub-partition), 8 for the optimized variant, whose U staged regions per
+// group cost shared memory and hence residency (U = 16 measured up to 2x
+// slower there). LMT_UMAX overrides both.
+int jit_umax(bool opt) {
+    if (const char *e = getenv("LMT_UMAX")) return atoi(e) >= 16 ? 16 : 8;
+    return opt ? 8 : 16;
 }
 
 bool jit_vec() {
@@ -421,12 +439,12 @@ int64_t jit_regs_guess(int K, int64_t slot, int U, int D) {
 void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_t warps, int64_t nit, int64_t sms,
                 bool opt, int64_t stage_bytes, int64_t smem_cap, int *U_out, int *D_out, int *S_out) {
     int bu = 1, bd = 3, bs = 1;
-    for (int U : {8, 4, 2, 1})
+    for (int U : {jit_umax(false), 8, 4, 2, 1})
         if (U <= nit) { bu = U; break; }
     if (opt) {
         bd = 2;  // shared-memory loads: one step of lookahead covers them
         double best = -1.0;
-        for (int U : {8, 4, 2, 1}) {
+        for (int U : {jit_umax(true), 8, 4, 2, 1}) {
             if (U > nit) continue;
             const int64_t slot = (int64_t)U * K + p.num_coal_ilb + p.num_uncoal_ilb;
             const int64_t regs = std::min<int64_t>(jit_regs_guess(K, slot, U, 2), 65536 / maxt);
@@ -448,7 +466,7 @@ void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_
     }
     if (const char *fu = getenv("LMT_FORCE_U")) {
         const int f = atoi(fu);
-        if (f == 1 || f == 2 || f == 4 || f == 8) bu = (int)std::min<int64_t>(f, std::max<int64_t>(1, nit));
+        if (f == 1 || f == 2 || f == 4 || f == 8 || f == 16) bu = (int)std::min<int64_t>(f, std::max<int64_t>(1, nit));
     }
     if (const char *fd = getenv("LMT_FORCE_D")) {
         const int f = atoi(fd);
@@ -871,7 +889,7 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         }
         m.alg_bytes = pl.alg_bytes;
         m.alg_flops = pl.alg_flops;
-        m.kernel_id = pl.jit ? 10000 + pl.kb.U * 1000 + pl.kb.D * 100 + pl.ko.U * 10 + pl.ko.D
+        m.kernel_id = pl.jit ? jit_kid(pl.kb, pl.ko)
                              : pl.sid * 100 + (pl.wide ? 50 : 0) + pl.u_base * 10 + pl.u_opt;
         cudaEvent_t *ev = &c->events[(size_t)i * 4];
         // ---- inputs (make_inputs, interp.py:30-38)
@@ -942,7 +960,7 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
             int jrc = g_jit.get(c->device, pl.kb, &f, &gb, &err);
             if (!jrc && !(flags & LMT_MEASURE_SKIP_OPT) && pl.feasible) jrc = g_jit.get(c->device, pl.ko, &f, &go, &err);
             if (jrc) { m.status = fail(LMT_ERR_CUDA, "%s", err.c_str()); continue; }
-            m.kernel_id = 10000 + gb.U * 1000 + gb.D * 100 + go.U * 10 + go.D;  // the kernels built
+            m.kernel_id = jit_kid(gb, go);  // the kernels built
         }
         CUDA_TRY(cudaEventRecord(ev[0], s));
         rc = launch_variant(pl, 0, c->in, rows, cols, pitch, c->in2, c->outb, s);
