@@ -33,18 +33,22 @@ def _args(argv=None):
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=256, help="instances per checkpoint")
     ap.add_argument("--limit", type=int, default=0, help="only the first N rows of this rank's share (testing)")
+    ap.add_argument("--sample", type=int, default=0, help="a seeded random subset of N rows of the selection")
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl with a GPU, else gloo)")
     return ap.parse_args(argv)
 
 
-def rank_share(table, world: int, rank: int) -> np.ndarray:
-    """Cost-balanced disjoint share of the whole selection (sorted rows)."""
+def rank_share(table, world: int, rank: int, sample: int = 0, seed: int = 0) -> np.ndarray:
+    """Cost-balanced disjoint share of the whole selection, or of a seeded
+    random subset of `sample` rows (sorted rows)."""
     from . import sweep
 
     rows = np.arange(len(table))
+    if sample and sample < len(rows):
+        rows = np.sort(np.random.default_rng(seed ^ 0x5A3B1E).choice(len(rows), size=sample, replace=False))
     if world == 1:
         return rows
-    cost = sweep.estimated_cost(table.records(rows))
+    cost = sweep.launch_cost(table.records(rows))
     return np.sort(rows[sweep.shard_balanced(cost, world)[rank]])
 
 
@@ -68,7 +72,7 @@ def run(argv=None) -> dict:
 
     spec = sweep.SamplingSpec(max_instances=args.max_instances, seed=args.seed)
     table = sweep.select_instance_table(spec)
-    mine = rank_share(table, world, rank)
+    mine = rank_share(table, world, rank, args.sample, args.seed)
     if args.limit:
         mine = mine[: args.limit]
     rdir = os.path.join(args.out, f"rank{rank:03d}")
