@@ -441,6 +441,18 @@ void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_
     int bu = 1, bd = 3, bs = 1;
     for (int U : {jit_umax(false), 8, 4, 2, 1})
         if (U <= nit) { bu = U; break; }
+    if (!opt) {
+        // start where the register estimate fits (ptxas has the last word in
+        // JitCache::resolve; a good start saves the compiles of the step-down)
+        const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
+        const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
+        auto est = [&](int U, int D) { return D * ((int64_t)U * K + ctx) + 48 + 4 * U + (16 * K) / 10; };
+        while (bu > 1 || bd > 1) {
+            if (est(bu, bd) <= regcap) break;
+            if (bd > 1) bd--;
+            else { bu >>= 1; bd = 3; }
+        }
+    }
     if (opt) {
         bd = 2;  // shared-memory loads: one step of lookahead covers them
         double best = -1.0;
