@@ -186,6 +186,7 @@ typedef struct exec_ctx {
     int K;
     int64_t wg_begin, wg_end;
     int64_t next;           /* shared work counter (under lock) */
+    int64_t budget;         /* > 0: stop after this many work units (timing samples) */
     pthread_mutex_t lock;
     int err;
 } exec_ctx;
@@ -225,6 +226,7 @@ static int run_workgroup(exec_ctx *x, int64_t gy, int64_t gx, float *region, flo
             }
             for (int64_t lane = 0; lane < wg_size; lane++) acc[lane] = 0.0f;
             for (int64_t lane = 0; lane < wg_size; lane++) {
+                if (x->budget > 0 && --x->budget == 0) return ORA_OK;
                 const int64_t wi_x = lane % wg_w, wi_y = lane / wg_w;
                 const int64_t glin = (gy * wg_h + wi_y) * p->grid_x + (gx * wg_w + wi_x);
                 const int64_t wu_x = wu_x0 + wi_x, wu_y = wu_y0 + wi_y;
@@ -487,4 +489,32 @@ void ora_real_mvt(const float *A, const float *y1, const float *y2, const float 
         x1[i] = a1;
         x2[i] = a2;
     }
+}
+
+/* Timing sample for the CPU baseline: workgroup 0 of `variant`, one thread,
+ * stopping after `max_units` work units. Returns the number done. */
+int64_t ora_execute_sample(const ora_instance *p, const ora_device *dev, int variant, const float *in,
+                           int64_t in_rows, int64_t in_cols, const float *in2, float *out, int64_t max_units) {
+    ora_geometry g;
+    if (ora_geometry_of(p, dev, &g) != ORA_OK || max_units < 1) return -1;
+    exec_ctx *x = (exec_ctx *)calloc(1, sizeof(exec_ctx));
+    x->p = p;
+    x->g = &g;
+    x->variant = variant;
+    x->in = in;
+    x->in_rows = in_rows;
+    x->in_cols = in_cols;
+    x->in2 = in2;
+    x->out = out;
+    x->K = ora_stencil_offsets(p->stencil_shape, p->stencil_radius, x->dr, x->dc, 1024);
+    x->budget = max_units + 1;
+    const int64_t wg_size = (int64_t)p->wg_x * p->wg_y;
+    float *region = variant == 1 ? (float *)malloc(sizeof(float) * (size_t)g.r_rows * (size_t)g.r_cols_pad) : NULL;
+    float *acc = (float *)malloc(sizeof(float) * (size_t)wg_size);
+    int rc = run_workgroup(x, 0, 0, region, acc);
+    const int64_t done = x->budget == 0 ? max_units : max_units + 1 - x->budget;
+    free(region);
+    free(acc);
+    free(x);
+    return rc == ORA_OK ? done : -1;
 }
