@@ -32,6 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SWEEP_CAP = 1_000_000
+# collectives: NCCL over NVLink between GPUs; LMT_DIST_BACKEND=gloo runs the
+# same multi-rank code with host tensors (e.g. several ranks on one GPU)
+BACKEND = os.environ.get("LMT_DIST_BACKEND", "nccl")
+COLL = "cuda" if BACKEND == "nccl" else "cpu"
 METRIC = "synthetic instances timed/sec (both variants)"
 UNIT = "instances/s"
 
@@ -218,6 +222,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
 
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     L, table, perm = workload(args.seed)
     from paper_1412_6986_b200 import _lib
@@ -256,9 +261,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
     barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
+    t = torch.tensor([elapsed_ms], device=COLL, dtype=torch.float64)
     n_local = sum(len(r) for r, _ in results)
-    cnt = torch.tensor([n_local], device="cuda", dtype=torch.float64)
+    cnt = torch.tensor([n_local], device=COLL, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
@@ -269,7 +274,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- labels: NCCL all-gather of (row, t_base, t_opt) -- the only collective
     rows_all = np.concatenate([r for r, _ in results])
     res_all = np.concatenate([x for _, x in results])
-    labels = L.dist.all_gather_labels(L.dist.label_matrix(rows_all, res_all), device="cuda")
+    labels = L.dist.all_gather_labels(L.dist.label_matrix(rows_all, res_all), device=COLL)
     n_labels = int(labels.shape[0])
 
     # ---- per-kernel accounting (the synthetic kernels are the dominant launches)
@@ -460,7 +465,7 @@ def run_rf(args, L, world, rank, barrier):
         os.unlink(tmpf.name)
         train_info = {"train_s": t_train, "train_rows": int(len(y)), "train_threads": min(20, os.cpu_count() or 1),
                       "trained_model_file_bitwise_reference": same}
-    t = torch.tensor([t_feat, t_k3, t_e2e], dtype=torch.float64, device="cuda")
+    t = torch.tensor([t_feat, t_k3, t_e2e], dtype=torch.float64, device=COLL)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_feat, t_k3, t_e2e = (float(v) for v in t.tolist())
@@ -537,7 +542,7 @@ def run_e2e(args, L, table, perm, world, rank, barrier):
     el = time.perf_counter() - t0
     import torch.distributed as dist
 
-    t = torch.tensor([el, float(n)], device="cuda", dtype=torch.float64)
+    t = torch.tensor([el, float(n)], device=COLL, dtype=torch.float64)
     if world > 1:
         mx = t[:1].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -562,8 +567,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # LMT_DIST_BACKEND=gloo: exercise the multi-rank path with several ranks on one GPU
+            dist.init_process_group(BACKEND)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
