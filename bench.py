@@ -181,6 +181,16 @@ def cpu_sample(L, table, rows, budget_s: float):
     return rate, cores, desc
 
 
+def bench_config(args, world: int) -> dict:
+    """The workload both arms report (BASELINE.json configs[4] at N ranks)."""
+    return {
+        "workload": f"full synthetic sweep SamplingSpec(max_instances={SWEEP_CAP}, seed={args.seed}); "
+                    f"each step a seeded-random batch of {args.batch} instances per rank (both variants each)",
+        "batch_per_rank": args.batch, "out": "2048x2048", "parallelism": f"dp{world} (cost-balanced shards)",
+        "l2": "per-step working set >> 126 MB L2 (each instance writes 2x16 MB outputs plus its inputs)",
+    }
+
+
 def fp32_peak_tflops():
     """fp32 FMA peak: measured by tools/probes/fp32_peak.cu on this pool's
     B200 (profiles/fp32_peak.json), else the nominal 148 SMs x 128 lanes x 2
@@ -208,8 +218,7 @@ def run_reference(args, rank: int, world: int):
         "warmup": args.warmup, "ms_per_step": (args.batch / value * 1e3) if value else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"full synthetic sweep SamplingSpec(max_instances={SWEEP_CAP}, seed={args.seed}), "
-                               f"batches of {args.batch} instances", "batch_per_rank": args.batch},
+        "config": bench_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -285,9 +294,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     k_flops = float(res_all["alg_flops"][ok].sum() + res_all["alg_flops"][ran_opt].sum())
     n_launch_kernels = int(ok.sum() + ran_opt.sum())
     fill_ms = float(res_all["t_fill_ms"].sum())
-    verified = int(((res_all["mismatches"] == 0) & ran_opt).sum())
-    mismatched = int(((res_all["mismatches"] > 0) & ran_opt).sum())
-    failed = int((~ok).sum())
+    counts = torch.tensor([((res_all["mismatches"] == 0) & ran_opt).sum(), ((res_all["mismatches"] > 0) & ran_opt).sum(),
+                           (~ok).sum(), int(res_all["launches"].sum())], device=COLL, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    verified, mismatched, failed, launches_all = (int(v) for v in counts.tolist())
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -298,7 +309,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     fp32_peak, fp32_src = fp32_peak_tflops()
     roof = L.measure.roofline(res_all, hbm_peak, fp32_peak)
     floor = L.measure.launch_floor(table.records(rows_all), res_all, hbm_peak)
-    gpu_launches = int(res_all["launches"].sum())
+    gpu_launches = launches_all
     if args.dump:
         np.savez(args.dump if world == 1 else f"{args.dump}.rank{rank}", rows=rows_all,
                  rec=table.records(rows_all), res=res_all)
@@ -321,12 +332,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {
-            "workload": f"full synthetic sweep SamplingSpec(max_instances={SWEEP_CAP}, seed={args.seed}); "
-                        f"each step a seeded-random batch of {args.batch} instances per rank (both variants each)",
-            "batch_per_rank": args.batch, "out": "2048x2048", "parallelism": f"dp{world} (cost-balanced shards)",
-            "l2": "per-step working set >> 126 MB L2 (each instance writes 2x16 MB outputs plus its inputs)",
-        },
+        "config": bench_config(args, world),
         "instances_timed": n_total, "labels_gathered": n_labels, "verified_bitwise": verified,
         "mismatched": mismatched, "failed": failed,
         "kernel_ms": k_ms, "fill_ms": fill_ms, "step_ms_total": max_ms,
