@@ -263,3 +263,34 @@ def test_run_sweep_checkpoint_resume_and_dataset(tmp_path):
     fb = L.features_records(table.records(lab["row"]))
     assert np.array_equal(np.stack([r.features.to_array() for r in rows]), fb.X)
     assert json.load(open(f"{out}/summary.json"))["total_rows"] == 24
+
+
+def _small(pat, n, m, shape, r, counts, out, grid, wg, inh=64):
+    params = L.TemplateParams(inh, inh, out[0], out[1], pat, n, m, L.StencilPattern(shape, r), **counts)
+    return L.KernelInstance(params, L.LaunchConfig(grid[0], grid[1], wg[0], wg[1]))
+
+
+def test_edge_paths_against_oracle():
+    """Kernel paths the golden set does not reach: context counts beyond the
+    in2 halo (ctx-wrap), regions wider than one 256-column TMA box (wide),
+    radius 3 stencils, in2 smaller than the halo, 1024-thread workgroups."""
+    P, S = L.HomeAccessPattern, L.StencilShape
+    base = dict(num_comp_ilb=3, num_comp_ep=2, num_coal_ilb=1, num_coal_ep=1, num_uncoal_ilb=1, num_uncoal_ep=1)
+    wrap = dict(num_comp_ilb=5, num_comp_ep=3, num_coal_ilb=20, num_coal_ep=18, num_uncoal_ilb=11, num_uncoal_ep=9)
+    cases = [
+        _small(P.XY_REUSE, 4, 4, S.RECTANGULAR, 1, wrap, (64, 64), (32, 32), (8, 8)),
+        _small(P.NO_REUSE_ROW_MAJOR, 2, 2, S.STAR, 2, wrap, (32, 32), (32, 32), (4, 8), inh=16),
+        _small(P.Y_REUSE_COL, 2, 4, S.RECTANGULAR, 1, base, (32, 512), (512, 2), (512, 1), inh=64),
+        _small(P.X_REUSE_COL, 4, 2, S.DIAMOND, 2, base, (512, 32), (2, 512), (1, 512), inh=64),
+        _small(P.NO_REUSE_COL_MAJOR, 2, 3, S.RECTANGULAR, 3, base, (32, 32), (32, 32), (8, 4)),
+        _small(P.Y_REUSE_ROW, 3, 2, S.STAR, 3, base, (64, 64), (32, 32), (32, 32)),
+        _small(P.XY_REUSE, 8, 8, S.DIAMOND, 0, base, (64, 64), (64, 16), (32, 16), inh=4),
+    ]
+    L.prepare_instances(cases)
+    for inst in cases:
+        base_out, opt_out = L.run_pair(inst)
+        want_b, _ = oracle.run_pair(inst)
+        assert np.array_equal(base_out, want_b), inst
+        assert np.array_equal(opt_out, want_b), inst
+        m = L.measure_instances([inst])[0]
+        assert m.verified and m.digest_base == oracle.out_hash(want_b)
