@@ -49,7 +49,7 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
     """The configs[1] instance set: 15 transpose (tile T in {8,16,32} x rows
     per CTA step), 14 matrixMul (T in {4..32} x outputs per thread), 24
     convolution (radius in {1,2,4,8} x 6 workgroups), 10 MVT (workgroup x
-    j-tile), plus 2 transpose and 4 convolution instances at 8192 x 8192
+    j-tile), plus 5 transpose and 4 convolution instances at 8192 x 8192
     (arrays well beyond L2) for the HBM roof."""
     out = []
     for T in (8, 16, 32):
@@ -67,7 +67,8 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
         for T in (16, 32):
             out.append(RealInstance(3, n_mvt, wg, 1, tile=T))
     # HBM-scale instances (8192^2: 256 MB per array, beyond L2) for the bandwidth roof
-    out.append(RealInstance(0, 8192, 32, 8, tile=32))
+    for wy in (1, 2, 4, 8):  # 32 .. 4 elements per thread in flight
+        out.append(RealInstance(0, 8192, 32, wy, tile=32))
     out.append(RealInstance(0, 8192, 16, 16, tile=16))
     for R in (1, 2, 4, 8):
         out.append(RealInstance(2, 8192, 32, 8, radius=R))
