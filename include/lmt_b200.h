@@ -189,7 +189,8 @@ int lmt_features(const lmt_instance *insts, int64_t n, const lmt_device *devs, i
  * (SPEC.md:15); semantics are defined in csrc/lmt_real.cuh and pinned by the
  * C oracle. kernel: 0 transpose, 1 matrixMul, 2 convolution-separable,
  * 3 MVT. tile: transpose / matrixMul tile (== wg_x; wg_y = tile / work per
- * thread), MVT j-tile; radius: convolution radius (1..16). */
+ * thread), MVT j-tile, convolution outputs per thread; radius: convolution
+ * radius (1..16). */
 typedef struct lmt_real_instance {
     int32_t kernel, n, wg_x, wg_y, tile, radius;
 } lmt_real_instance;

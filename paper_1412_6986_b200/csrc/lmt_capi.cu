@@ -1167,7 +1167,8 @@ std::string real_violations(const lmt_real_instance &r) {
             if (T / wy != 1 && T / wy != 2 && T / wy != 4 && T / wy != 8) return "matrixMul work per thread tile/wg_y must be 1, 2, 4 or 8";
             return "";
         case 2:
-            if (n % wx || n % wy) return "convolution needs wg_x | n and wg_y | n";
+            if (T < 1) return "convolution outputs per thread (tile) must be >= 1";
+            if (n % (wx * T) || n % (wy * T)) return "convolution needs wg_x * tile | n and wg_y * tile | n";
             if (r.radius < 1 || r.radius > kConvMaxRadius) return "convolution radius must be in [1, 16]";
             return "";
         case 3:
@@ -1214,15 +1215,15 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
             break;
         }
         case 2: {
-            const dim3 grd(n / wx, n / wy);
             const RealConv c = real_weights(r.radius);
-            const int R = r.radius;
+            const int R = r.radius, W = T;
+            const dim3 grr(n / (wx * W), n / wy), grc(n / wx, n / (wy * W));
             if (variant == 0) {
-                k_conv_rows_base<<<grd, blk, 0, s>>>(in[0], tmp, n, R, c);
-                k_conv_cols_base<<<grd, blk, 0, s>>>(tmp, out, n, R, c);
+                k_conv_rows_base<<<grr, blk, 0, s>>>(in[0], tmp, n, R, W, c);
+                k_conv_cols_base<<<grc, blk, 0, s>>>(tmp, out, n, R, W, c);
             } else {
-                k_conv_rows_opt<<<grd, blk, (size_t)wy * (wx + 2 * R) * 4, s>>>(in[0], tmp, n, R, c);
-                k_conv_cols_opt<<<grd, blk, (size_t)(wy + 2 * R) * wx * 4, s>>>(tmp, out, n, R, c);
+                k_conv_rows_opt<<<grr, blk, (size_t)wy * (W * wx + 2 * R) * 4, s>>>(in[0], tmp, n, R, W, c);
+                k_conv_cols_opt<<<grc, blk, (size_t)(W * wy + 2 * R) * wx * 4, s>>>(tmp, out, n, R, W, c);
             }
             break;
         }

@@ -93,56 +93,76 @@ __global__ void k_matmul_opt(const float *__restrict__ A, const float *__restric
 
 // ------------------------------------------------------------ convolution-separable
 // rows: out[y][x] = sum_{k=-R..R} in[y][x+k] * w[R-k]; cols: out[y][x] = sum_k in[y+k][x] * w[R-k];
-// taps outside the image read 0; blockDim (wx, wy), one output per thread.
-__global__ void k_conv_rows_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
-    float acc = 0.0f;
-    for (int k = -R; k <= R; ++k) {
-        const int xx = x + k;
-        const float v = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
-        acc = __fmaf_rn(v, c.w[R - k], acc);
+// taps outside the image read 0. blockDim (wx, wy); each thread computes W
+// outputs, blockDim apart along the pass direction (the tiling factor: W
+// independent loads in flight per tap).
+__global__ void k_conv_rows_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+                                 RealConv c) {
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int x0 = blockIdx.x * blockDim.x * W + threadIdx.x;
+    for (int q = 0; q < W; ++q) {
+        const int x = x0 + q * blockDim.x;
+        float acc = 0.0f;
+        for (int k = -R; k <= R; ++k) {
+            const int xx = x + k;
+            const float v = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
+            acc = __fmaf_rn(v, c.w[R - k], acc);
+        }
+        out[(size_t)y * n + x] = acc;
     }
-    out[(size_t)y * n + x] = acc;
 }
 
-__global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
-    float acc = 0.0f;
-    for (int k = -R; k <= R; ++k) {
-        const int yy = y + k;
-        const float v = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
-        acc = __fmaf_rn(v, c.w[R - k], acc);
+__global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+                                 RealConv c) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y0 = blockIdx.y * blockDim.y * W + threadIdx.y;
+    for (int q = 0; q < W; ++q) {
+        const int y = y0 + q * blockDim.y;
+        float acc = 0.0f;
+        for (int k = -R; k <= R; ++k) {
+            const int yy = y + k;
+            const float v = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
+            acc = __fmaf_rn(v, c.w[R - k], acc);
+        }
+        out[(size_t)y * n + x] = acc;
     }
-    out[(size_t)y * n + x] = acc;
 }
 
-// optimized: the CTA's rows plus the apron staged once in shared memory
-__global__ void k_conv_rows_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
-    extern __shared__ float s[];  // [wy][wx + 2R]
-    const int wx = blockDim.x, wy = blockDim.y, P = wx + 2 * R;
-    const int x0 = blockIdx.x * wx - R, y = blockIdx.y * wy + threadIdx.y;
+// optimized: the CTA's rows (its W * wx columns plus the apron) staged once in shared memory
+__global__ void k_conv_rows_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+                                RealConv c) {
+    extern __shared__ float s[];  // [wy][W * wx + 2R]
+    const int wx = blockDim.x, wy = blockDim.y, P = W * wx + 2 * R;
+    const int x0 = blockIdx.x * wx * W - R, y = blockIdx.y * wy + threadIdx.y;
     for (int t = threadIdx.x; t < P; t += wx) {
         const int xx = x0 + t;
         s[threadIdx.y * P + t] = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
     }
     __syncthreads();
-    float acc = 0.0f;
-    for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[threadIdx.y * P + threadIdx.x + R + k], c.w[R - k], acc);
-    out[(size_t)y * n + blockIdx.x * wx + threadIdx.x] = acc;
+    for (int q = 0; q < W; ++q) {
+        const int lx = threadIdx.x + q * wx;
+        float acc = 0.0f;
+        for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[threadIdx.y * P + lx + R + k], c.w[R - k], acc);
+        out[(size_t)y * n + blockIdx.x * wx * W + lx] = acc;
+    }
 }
 
-__global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, RealConv c) {
-    extern __shared__ float s[];  // [wy + 2R][wx]
-    const int wx = blockDim.x, wy = blockDim.y, H = wy + 2 * R;
-    const int x = blockIdx.x * wx + threadIdx.x, y0 = blockIdx.y * wy - R;
+__global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+                                RealConv c) {
+    extern __shared__ float s[];  // [W * wy + 2R][wx]
+    const int wx = blockDim.x, wy = blockDim.y, H = W * wy + 2 * R;
+    const int x = blockIdx.x * wx + threadIdx.x, y0 = blockIdx.y * wy * W - R;
     for (int t = threadIdx.y; t < H; t += wy) {
         const int yy = y0 + t;
         s[t * wx + threadIdx.x] = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
     }
     __syncthreads();
-    float acc = 0.0f;
-    for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[(threadIdx.y + R + k) * wx + threadIdx.x], c.w[R - k], acc);
-    out[(size_t)(blockIdx.y * wy + threadIdx.y) * n + x] = acc;
+    for (int q = 0; q < W; ++q) {
+        const int ly = threadIdx.y + q * wy;
+        float acc = 0.0f;
+        for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[(ly + R + k) * wx + threadIdx.x], c.w[R - k], acc);
+        out[(size_t)(blockIdx.y * wy * W + ly) * n + x] = acc;
+    }
 }
 
 // ------------------------------------------------------------ MVT (Polybench)

@@ -28,7 +28,7 @@ class RealInstance:
     n: int           # square problem size
     wg_x: int
     wg_y: int
-    tile: int = 0    # transpose / matrixMul tile (== wg_x), MVT j-tile
+    tile: int = 0    # transpose / matrixMul tile (== wg_x), MVT j-tile, convolution outputs per thread
     radius: int = 0  # convolution radius
 
     @property
@@ -49,7 +49,7 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
     """The configs[1] instance set: 15 transpose (tile T in {8,16,32} x rows
     per CTA step), 14 matrixMul (T in {4..32} x outputs per thread), 24
     convolution (radius in {1,2,4,8} x 6 workgroups), 10 MVT (workgroup x
-    j-tile), plus 5 transpose and 4 convolution instances at 8192 x 8192
+    j-tile), plus 5 transpose and 8 convolution instances at 8192 x 8192
     (arrays well beyond L2) for the HBM roof."""
     out = []
     for T in (8, 16, 32):
@@ -62,7 +62,7 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
                 out.append(RealInstance(1, n_matmul, T, T // W, tile=T))
     for R in (1, 2, 4, 8):
         for wx, wy in ((16, 4), (32, 4), (32, 8), (64, 4), (128, 1), (16, 16)):
-            out.append(RealInstance(2, n_conv, wx, wy, radius=R))
+            out.append(RealInstance(2, n_conv, wx, wy, tile=1, radius=R))
     for wg in (32, 64, 128, 256, 512):
         for T in (16, 32):
             out.append(RealInstance(3, n_mvt, wg, 1, tile=T))
@@ -71,7 +71,8 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
         out.append(RealInstance(0, 8192, 32, wy, tile=32))
     out.append(RealInstance(0, 8192, 16, 16, tile=16))
     for R in (1, 2, 4, 8):
-        out.append(RealInstance(2, 8192, 32, 8, radius=R))
+        for W in (1, 4):  # outputs per thread
+            out.append(RealInstance(2, 8192, 32, 8, tile=W, radius=R))
     return out
 
 
