@@ -626,14 +626,26 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
                              p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
         JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
                   p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
-                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf(), 0};
+                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf(), 0, 1};
         // 128-bit stencil-row loads in the baseline need rows of >= 5 taps (radius >= 2)
         k0.vec = (p.stencil_radius >= 2 && jit_vec()) ? 1 : 0;
         int Ub, Db, Uo, Do, Sb, So;
-        choose_jit(K, p, maxt, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
+        // Baseline launches with few work units per thread (U <= 2) and CTAs to
+        // spare get their ILP from resident warps instead: launch bounds that
+        // keep 32 warps per SM resident (8 per scheduler) cap the registers.
+        int64_t maxt_b = maxt, minb = 1;
+        if (nit <= 2 && ctas >= 2 * sms && !getenv("LMT_NO_MINB")) {
+            minb = std::min<int64_t>({(32 + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
+                                      ctas / std::max<int64_t>(1, sms)});
+            if (minb > 1) maxt_b = warps * 32;
+            else minb = 1;
+        }
+        choose_jit(K, p, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
         choose_jit(K, p, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
         S = So;
         pl->kb = k0;
+        pl->kb.maxt = (int)maxt_b;
+        pl->kb.minb = (int)minb;
         pl->kb.U = Ub;
         pl->kb.D = Db;
         pl->ko = k0;

@@ -32,6 +32,7 @@
 //   LMT_WIDE                             optimized variant with several 256-column TMA chunks
 //   LMT_CTXWRAP                          context counts exceed the in2 halo: reduce indices mod IN2_H/W
 //   LMT_VEC                              baseline: 128-bit loads for stencil rows of >= 5 taps
+//   LMT_MAXT LMT_MINB                    launch bounds (max threads per CTA, min resident CTAs per SM)
 //   LMT_PF                               L1 prefetch distance in steps for the in2 context lines (0 off)
 //   LMT_H2 LMT_W2 LMT_P2                 in2 shape (IN2_H, IN2_W: #defines in the reference too) and
 //                                        its physical pitch, so every context read of a step is
@@ -442,7 +443,7 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, Src src, const flo
 #if !LMT_OPT
 // blockDim = (WG_W, WG_H), gridDim = (GRID_X/WG_W, GRID_Y/WG_H); work units
 // blocked across workgroups, cyclic across workitems (kernel_model.py:158-170).
-extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1) lmt_kernel(const SynthArgs A) {
+extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB) lmt_kernel(const SynthArgs A) {
     const int wi_x = threadIdx.x, wi_y = threadIdx.y;
     const int wg_w = blockDim.x, wg_h = blockDim.y;
     const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
