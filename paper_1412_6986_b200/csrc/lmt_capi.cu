@@ -446,7 +446,9 @@ void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_
         // JitCache::resolve; a good start saves the compiles of the step-down)
         const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
         const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
-        auto est = [&](int U, int D) { return D * ((int64_t)U * K + ctx) + 48 + 4 * U + (16 * K) / 10; };
+        // a lower bound (values in flight + a little): prunes only configs
+        // that cannot fit; the spill check decides the rest
+        auto est = [&](int U, int D) { return D * ((int64_t)U * K + ctx) + 16; };
         while (bu > 1 || bd > 1) {
             if (est(bu, bd) <= regcap) break;
             if (bd > 1) bd--;
