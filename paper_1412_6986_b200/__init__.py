@@ -9,7 +9,7 @@ liblmt_b200.so (hand-written sm_100a CUDA behind a C ABI, include/lmt_b200.h);
 there is no CPU fallback.
 """
 
-from . import access_analysis, codegen, cost_model, dataset, dist, measure, metrics, real, sweep  # noqa: F401
+from . import access_analysis, codegen, cost_model, dataset, dist, measure, metrics, real, study, sweep  # noqa: F401
 from .access_analysis import (
     FEATURE_NAMES,
     FeatureVector,

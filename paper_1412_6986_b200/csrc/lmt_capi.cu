@@ -806,6 +806,9 @@ int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, co
                 int64_t in_cols, int64_t in_pitch, const float *d_in2, float *d_out, void *stream) {
     if (!inst || !d_in || !d_in2 || !d_out) return fail(LMT_ERR_ARG, "null argument");
     if (variant != 0 && variant != 1) return fail(LMT_ERR_ARG, "variant must be 0 or 1");
+    // the 128-bit row loads and the TMA descriptor need 16-byte rows
+    if (in_pitch % 4 || reinterpret_cast<uintptr_t>(d_in) % 16)
+        return fail(LMT_ERR_ARG, "in pitch must be a multiple of 4 floats and the base 16-byte aligned");
     std::lock_guard<std::mutex> lk(g_mu);
     DevCtx *c;
     int rc = get_ctx(&c);

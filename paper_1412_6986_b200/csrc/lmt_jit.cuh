@@ -163,13 +163,16 @@ struct GlobalSrc {
 #pragma unroll
         for (int u = 0; u < NU_; ++u) {
             const float *q = p[u];
+            const int qa = (int)(reinterpret_cast<unsigned long long>(q) >> 2);
 #pragma unroll
             for (int dr = -RAD; dr <= RAD; ++dr) {
                 const int w = row_w(dr), k0 = row_first(dr), nt = 2 * w + 1;
                 if (LMT_VEC && nt >= 5) {
-                    const float *st = q + (dr * pitch - w);
-                    const int sh = (int)(reinterpret_cast<unsigned long long>(st) >> 2) & 3;
-                    const float4 *vp = reinterpret_cast<const float4 *>(st + ((long long)sh * cs - sh));
+                    // the copy is the same for every row of the unit (pitch % 4 == 0):
+                    // one shifted base per unit and row width, rows as offsets of it
+                    const int sh = (qa - w) & 3;
+                    const float4 *vp =
+                        reinterpret_cast<const float4 *>(q + ((long long)sh * cs - sh - w) + dr * pitch);
 #pragma unroll
                     for (int b = 0; b < (nt + 3) / 4; ++b) {
                         const float4 x = __ldg(vp + b);

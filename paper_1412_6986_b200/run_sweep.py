@@ -13,7 +13,10 @@ collective), chunk files DIR/rank{r:03d}/chunk{k:06d}.npz written atomically
 labels are all-gathered (NCCL on GPUs, the only collective) and rank 0 writes
 DIR/labels.npz; every rank writes its rows of the 39-column dataset CSV
 (DIR/dataset.shardRRR-of-WWW.csv, dataset.py:284-341), and rank 0 merges them
-into DIR/dataset.csv in the reference's row order.
+into DIR/dataset.csv in the reference's row order. With --study, the
+paper's random-forest study follows on the gathered labels (study.py: every
+rank trains the same forests, predicts its own held-out rows, rank 0 scores
+them into DIR/study.json).
 """
 
 from __future__ import annotations
@@ -35,6 +38,8 @@ def _args(argv=None):
     ap.add_argument("--limit", type=int, default=0, help="only the first N rows of this rank's share (testing)")
     ap.add_argument("--sample", type=int, default=0, help="a seeded random subset of N rows of the selection")
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl with a GPU, else gloo)")
+    ap.add_argument("--study", action="store_true",
+                    help="after the gather: the paper's RF study on modelled and measured labels (study.py)")
     return ap.parse_args(argv)
 
 
@@ -56,7 +61,7 @@ def run(argv=None) -> dict:
     import torch
     import torch.distributed as dist
 
-    from . import dataset, dist as ldist, measure, sweep
+    from . import dataset, dist as ldist, measure, study, sweep
     from .access_analysis import features_records
 
     args = _args(argv)
@@ -65,10 +70,11 @@ def run(argv=None) -> dict:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cuda = torch.cuda.is_available()
     if cuda:
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(local % torch.cuda.device_count())  # ranks may share a GPU (tests)
+    backend = args.backend or ("nccl" if cuda else "gloo")
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group(args.backend or ("nccl" if cuda else "gloo"))
-    device = "cuda" if cuda else None
+        dist.init_process_group(backend)
+    device = "cuda" if cuda and backend == "nccl" else None  # where the label gather's buffers live
 
     spec = sweep.SamplingSpec(max_instances=args.max_instances, seed=args.seed)
     table = sweep.select_instance_table(spec)
@@ -118,10 +124,15 @@ def run(argv=None) -> dict:
     lab = ldist.label_matrix(rows_all, res_all)
     extra = np.stack([res_all["mismatches"].astype(np.float64), res_all["status"].astype(np.float64)], 1)
     labels = ldist.all_gather_labels(np.concatenate([lab, extra], 1), device=device)
-    summary = {"rank": rank, "world": world, "rows": int(len(mine)), "chunks_resumed": resumed,
+    summary = {"rank": rank, "world": world, "max_instances": args.max_instances, "seed": args.seed,
+               "rows": int(len(mine)), "chunks_resumed": resumed,
                "prepare_s": t_prep, "measure_s": t_meas,
                "mismatched": int((res_all["mismatches"] > 0).sum()),
                "verified": int((res_all["mismatches"] == 0).sum())}
+    if args.study:  # every rank trains the same forests, predicts the held-out rows it measured
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        threads = max(1, (os.cpu_count() or 1) // max(1, local_world))
+        summary["study"] = study.run_rank(args.out, table, labels, rows_all, rank, args.seed, threads)
     if rank == 0:
         if world > 1:
             dist.barrier()
@@ -133,6 +144,8 @@ def run(argv=None) -> dict:
         np.savez(os.path.join(args.out, "labels.npz"), row=row, t_base_ms=tb, t_opt_ms=to,
                  measured_speedup=measured, mismatches=labels[:, 3], status=labels[:, 4])
         summary.update(total_rows=int(len(row)), dataset_rows=n)
+        if args.study:
+            summary["study_result"] = study.merge(args.out, table, labels, world, args.seed)
         with open(os.path.join(args.out, "summary.json"), "w") as fh:
             json.dump(summary, fh, indent=1)
     elif world > 1:

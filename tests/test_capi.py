@@ -35,6 +35,20 @@ def test_version_and_validation_without_gpu():
     assert n == 1 and buf.value == b"grid size 256 < 512"
 
 
+def test_execute_rejects_unaligned_in_without_gpu():
+    """lmt_execute's argument contract (include/lmt_b200.h): the in pitch is a
+    multiple of 4 floats and the base 16-byte aligned, checked before any
+    device work."""
+    from paper_1412_6986_b200 import _lib
+
+    L = _lib.lib()
+    rec = _lib.CInstance(1024, 1024, 1024, 1024, 5, 1, 1, 2, 1, 0, 0, 0, 0, 0, 0, 1024, 1024, 16, 16)
+    fake = ctypes.c_void_p(1 << 20)
+    for pitch, base in ((1042, 1 << 20), (1040, (1 << 20) + 4)):
+        rc = L.lmt_execute(ctypes.byref(rec), None, 0, ctypes.c_void_p(base), 1026, 1026, pitch, fake, fake, None)
+        assert rc == 4 and b"pitch" in L.lmt_last_error()
+
+
 def test_struct_layouts_match_header():
     from paper_1412_6986_b200 import _lib
 

@@ -70,3 +70,69 @@ def test_two_rank_shard_and_label_gather(tmp_path):
     # LPT bound: no share exceeds the mean by more than the largest single instance
     assert max(cost) <= sum(cost) / 2 + per.max() + 1e-12
     del torch
+
+
+def _fake_study_set(table, labels):
+    """Stand-in for study.study_set (K4 needs the GPU): deterministic rows,
+    features and both label kinds from the gathered rows."""
+    rows = np.sort(labels[:, 0].astype(np.int64))
+    rng = np.random.default_rng(11)
+    X = np.round(rng.uniform(0, 64, size=(len(rows), 18)))
+    modelled = 2.0 ** (X[:, 0] / 16 - 2 + (X[:, 3] > 32))
+    measured = np.where(rows % 7 == 0, 0.0, 2.0 ** (X[:, 1] / 32 - 1))
+    return rows, X, modelled, measured
+
+
+def _cpu_predict(forest, X):
+    import oracle
+
+    return 2.0 ** oracle.forest_mean(forest.trees, np.asarray(X, dtype=np.float64), nthreads=1)
+
+
+def _study_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import paper_1412_6986_b200 as L
+
+    L.study.study_set = _fake_study_set
+    L.forest.predict = _cpu_predict
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rows = np.arange(400)
+        mine = rows[rank::world]  # any disjoint cover
+        labels = np.stack([rows.astype(np.float64)] + [np.zeros(400)] * 4, 1)
+        L.study.run_rank(out_dir, None, labels, mine, rank, seed=5, threads=2)
+        if world > 1:
+            dist.barrier()
+        if rank == 0:
+            L.study.merge(out_dir, None, labels, world, seed=5)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+def test_two_rank_study_matches_one_rank(tmp_path):
+    """study.py's distributed form (SURVEY 8(e) "after the gather"): two gloo
+    ranks each predict their own held-out rows; rank 0's merged scores equal
+    a one-rank run's."""
+    pytest.importorskip("torch")
+    import json
+
+    import torch.multiprocessing as mp
+
+    one, two = tmp_path / "one", tmp_path / "two"
+    one.mkdir()
+    two.mkdir()
+    mp.start_processes(_study_worker, args=(1, 0, str(one)), nprocs=1, join=True, start_method="spawn")
+    mp.start_processes(_study_worker, args=(2, _free_port(), str(two)), nprocs=2, join=True, start_method="spawn")
+    a = json.load(open(one / "study.json"))
+    b = json.load(open(two / "study.json"))
+    assert a["ranks"] == 1 and b["ranks"] == 2
+    a.pop("ranks"), b.pop("ranks")
+    assert a == b
+    assert a["held_out"] == 360 and a["train"] == 40
+    for k in ("modelled_labels", "measured_labels"):
+        assert 0.0 <= a[k]["count_accuracy"] <= 1.0 and sum(a[k]["confusion"]) == 360

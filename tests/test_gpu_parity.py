@@ -2,12 +2,14 @@
 of the reference and against the CPU oracle. Bit-exact for every fp32 output
 (+-inf included), bit-exact fp64 RF means, bit-identical predictions."""
 
+import os
+
 import numpy as np
 import pytest
 
 import oracle
 import paper_1412_6986_b200 as L
-from conftest import GOLDEN_DIR, make_instance
+from conftest import GOLDEN_DIR, ROOT, make_instance
 
 pytestmark = pytest.mark.gpu
 
@@ -263,6 +265,29 @@ def test_run_sweep_checkpoint_resume_and_dataset(tmp_path):
     fb = L.features_records(table.records(lab["row"]))
     assert np.array_equal(np.stack([r.features.to_array() for r in rows]), fb.X)
     assert json.load(open(f"{out}/summary.json"))["total_rows"] == 24
+
+
+def test_run_sweep_study_two_ranks_match_one(tmp_path):
+    """run_sweep --study (SURVEY 8(e) after the gather): one rank, then two
+    ranks on this GPU over gloo (torchrun), on the same 32-instance sample --
+    the same study.json; every held-out row predicted by exactly one rank."""
+    import json
+    import subprocess
+    import sys
+
+    common = ["--max-instances", "3000", "--seed", "2", "--sample", "32", "--chunk", "8", "--study"]
+    one, two = str(tmp_path / "one"), str(tmp_path / "two")
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    subprocess.run([sys.executable, "-m", "paper_1412_6986_b200.run_sweep", "--out", one] + common,
+                   check=True, cwd=ROOT, env=env, timeout=900)
+    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                    "--master-addr", "127.0.0.1", "--master-port", "29533", "-m", "paper_1412_6986_b200.run_sweep",
+                    "--out", two, "--backend", "gloo"] + common, check=True, cwd=ROOT, env=env, timeout=900)
+    a, b = json.load(open(f"{one}/study.json")), json.load(open(f"{two}/study.json"))
+    assert (a.pop("ranks"), b.pop("ranks")) == (1, 2)
+    assert a == b and a["rows"] == 32 and a["train"] + a["held_out"] == 32
+    idx = [np.load(f"{two}/rank{r:03d}/study_pred.npz")["idx"] for r in range(2)]
+    assert len(np.intersect1d(*idx)) == 0 and len(idx[0]) + len(idx[1]) == a["held_out"]
 
 
 def _small(pat, n, m, shape, r, counts, out, grid, wg, inh=64):
