@@ -432,12 +432,27 @@ bool jit_enabled() {
 // overlap the next group's TMA with the current group), and shared memory
 // bounds residency: score = independent chains per SM sub-partition, then
 // TMA overlap, then U, then D.
+constexpr double kLoopInstrBudget = 2100.0;
+
 int64_t jit_regs_guess(int K, int64_t slot, int U, int D) {
     return std::min<int64_t>(255, D * slot + 100 + 6 * U + K);
 }
 
-void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_t warps, int64_t nit, int64_t sms,
-                bool opt, int64_t stage_bytes, int64_t smem_cap, int *U_out, int *D_out, int *S_out) {
+// Whether the U work units of an aligned group (iterations it0 .. it0+U-1,
+// it0 % U == 0) read identical `in` values: their home coordinates do not
+// depend on wu_x (a0 = a4 = 0) and either not on wu_y either (xy_reuse) or
+// the group lies in one row of work units (nwx % U == 0, or one row).
+bool jit_share(const SynthArgs &A, int U) {
+    if (U <= 1 || A.a[0] != 0 || A.a[4] != 0) return false;
+    if (const char *e = getenv("LMT_SHARE"); e && e[0] == '0') return false;
+    return (A.a[1] == 0 && A.a[5] == 0) || A.nwy == 1 || A.nwx % U == 0;
+}
+
+void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, int64_t ctas, int64_t warps,
+                int64_t nit, int64_t sms, bool opt, int64_t stage_bytes, int64_t smem_cap, int *U_out, int *D_out,
+                int *S_out) {
+    // stencil value sets a step holds for U work units
+    auto sets = [&](int U) -> int64_t { return jit_share(A, U) ? 1 : U; };
     int bu = 1, bd = 3, bs = 1;
     for (int U : {jit_umax(false), 8, 4, 2, 1})
         if (U <= nit) { bu = U; break; }
@@ -448,7 +463,7 @@ void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_
         const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
         // a lower bound (values in flight + a little): prunes only configs
         // that cannot fit; the spill check decides the rest
-        auto est = [&](int U, int D) { return D * ((int64_t)U * K + ctx) + 16; };
+        auto est = [&](int U, int D) { return D * (sets(U) * K + ctx) + U + 16; };
         while (bu > 1 || bd > 1) {
             if (est(bu, bd) <= regcap) break;
             if (bd > 1) bd--;
@@ -460,7 +475,7 @@ void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_
         double best = -1.0;
         for (int U : {jit_umax(true), 8, 4, 2, 1}) {
             if (U > nit) continue;
-            const int64_t slot = (int64_t)U * K + p.num_coal_ilb + p.num_uncoal_ilb;
+            const int64_t slot = sets(U) * K + p.num_coal_ilb + p.num_uncoal_ilb;
             const int64_t regs = std::min<int64_t>(jit_regs_guess(K, slot, U, 2), 65536 / maxt);
             const int64_t rregs = (regs + 7) / 8 * 8;
             for (int Sx : {2 * U, U}) {
@@ -477,6 +492,17 @@ void choose_jit(int K, const lmt_instance &p, int64_t maxt, int64_t ctas, int64_
                 if (score > best) { best = score; bu = U; bs = (int)S; }
             }
         }
+    }
+    // The steady-state loop is D unrolled steps of ~U * (K + comp + ctx)
+    // instructions. Past the 32 KB instruction cache (~2,000 SASS
+    // instructions) the loop runs up to 2x slower (measured on B200,
+    // tools/gpu_icache.sh: a 2,600-instruction body vs 1,300), so D is capped.
+    {
+        const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
+        auto step_instr = [&](int U) {
+            return 1.1 * U * (K + p.num_comp_ilb + ctx) + (jit_share(A, U) ? 0.0 : 0.8 * U * K) + ctx;
+        };
+        while (bd > 1 && bd * step_instr(bu) > kLoopInstrBudget) bd--;
     }
     if (const char *fu = getenv("LMT_FORCE_U")) {
         const int f = atoi(fu);
@@ -628,7 +654,7 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
                              p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
         JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
                   p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
-                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf(), 0, 1};
+                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf(), 0, 1, 0};
         // 128-bit stencil-row loads in the baseline need rows of >= 5 taps (radius >= 2)
         k0.vec = (p.stencil_radius >= 2 && jit_vec()) ? 1 : 0;
         int Ub, Db, Uo, Do, Sb, So;
@@ -642,18 +668,20 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
             if (minb > 1) maxt_b = warps * 32;
             else minb = 1;
         }
-        choose_jit(K, p, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
-        choose_jit(K, p, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
+        choose_jit(K, p, A, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
+        choose_jit(K, p, A, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
         S = So;
         pl->kb = k0;
         pl->kb.maxt = (int)maxt_b;
         pl->kb.minb = (int)minb;
         pl->kb.U = Ub;
         pl->kb.D = Db;
+        pl->kb.share = jit_share(A, Ub) ? 1 : 0;  // stays valid when the spill step-down halves U
         pl->ko = k0;
         pl->ko.U = Uo;
         pl->ko.D = Do;
         pl->ko.opt = 1;
+        pl->ko.share = jit_share(A, Uo) ? 1 : 0;
         pl->ko.wide = pl->wide ? 1 : 0;
         pl->u_base = Ub;
         pl->u_opt = Uo;

@@ -34,6 +34,10 @@
 //   LMT_VEC                              baseline: 128-bit loads for stencil rows of >= 5 taps
 //   LMT_MAXT LMT_MINB                    launch bounds (max threads per CTA, min resident CTAs per SM)
 //   LMT_PF                               L1 prefetch distance in steps for the in2 context lines (0 off)
+//   LMT_SHARE                            the U work units of a group read the same `in` values (their
+//                                        home coordinates do not depend on the work unit within the
+//                                        group: xy_reuse, or x_reuse_* with the group inside one row of
+//                                        work units), so a step loads them once for all U
 //   LMT_H2 LMT_W2 LMT_P2                 in2 shape (IN2_H, IN2_W: #defines in the reference too) and
 //                                        its physical pitch, so every context read of a step is
 //                                        one base register plus an immediate offset
@@ -43,6 +47,10 @@ namespace lmt {
 constexpr int SHAPE = LMT_SHAPE, RAD = LMT_R;
 constexpr int CI = LMT_CI, CE = LMT_CE, NC = LMT_NC, NCE = LMT_NCE, NU = LMT_NU, NUE = LMT_NUE;
 constexpr int U = LMT_U, D = LMT_D;
+constexpr bool SHARE = LMT_SHARE != 0;
+// stencil value sets a step loads for NU_ work units
+template <int NU_>
+constexpr int kSets = SHARE ? 1 : NU_;
 constexpr int kMaxStagesJ = 16;
 constexpr int H2 = LMT_H2, W2 = LMT_W2, P2 = LMT_P2;
 constexpr int PF = LMT_PF;
@@ -159,9 +167,9 @@ struct GlobalSrc {
     int pitch;
     long long cs;       // floats between copies of `in`
     template <int NU_>
-    __device__ __forceinline__ void load(float (&v)[NU_][KT]) const {
+    __device__ __forceinline__ void load(float (&v)[kSets<NU_>][KT]) const {
 #pragma unroll
-        for (int u = 0; u < NU_; ++u) {
+        for (int u = 0; u < kSets<NU_>; ++u) {
             const float *q = p[u];
             const int qa = (int)(reinterpret_cast<unsigned long long>(q) >> 2);
 #pragma unroll
@@ -206,10 +214,10 @@ struct SmemSrc {
     int pitch;
     int r = 0, c = 0;   // home-coordinate offset of the step being loaded next
     template <int NU_>
-    __device__ __forceinline__ void load(float (&v)[NU_][KT]) const {
+    __device__ __forceinline__ void load(float (&v)[kSets<NU_>][KT]) const {
         const int off = r * pitch + c;  // 32-bit shared addresses: recomputing is cheaper than more live pointers
 #pragma unroll
-        for (int u = 0; u < NU_; ++u) {
+        for (int u = 0; u < kSets<NU_>; ++u) {
             const float *q = p[u] + off;
 #pragma unroll
             for (int dr = -RAD; dr <= RAD; ++dr) {
@@ -232,9 +240,9 @@ struct SmemWideSrc {
     int hr[U], hc[U];      // region coordinate of the step being loaded next, per work unit
     int chunk;             // rows_padded * 256
     template <int NU_>
-    __device__ __forceinline__ void load(float (&v)[NU_][KT]) const {
+    __device__ __forceinline__ void load(float (&v)[kSets<NU_>][KT]) const {
 #pragma unroll
-        for (int u = 0; u < NU_; ++u) {
+        for (int u = 0; u < kSets<NU_>; ++u) {
 #pragma unroll
             for (int k = 0; k < KT; ++k) {
                 const int row = hr[u] + tap_dr(k), col = hc[u] + tap_dc(k);
@@ -259,7 +267,7 @@ constexpr int NUs = NU > 0 ? NU : 1;
 
 template <int NU_>
 struct Slot {
-    float v[NU_][KT];
+    float v[kSets<NU_>][KT];
     float c[NCs];
     float w[NUs];
 };
@@ -362,7 +370,7 @@ __device__ __forceinline__ void consume(float (&acc)[NU_], const Slot<NU_> &s) {
 #pragma unroll
     for (int k = 0; k < KT; ++k)
 #pragma unroll
-        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], s.v[u][k]);
+        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], s.v[SHARE ? 0 : u][k]);
 #pragma unroll
     for (int k = 0; k < CI; ++k)
 #pragma unroll

@@ -285,9 +285,17 @@ def test_run_sweep_study_two_ranks_match_one(tmp_path):
                     "--out", two, "--backend", "gloo"] + common, check=True, cwd=ROOT, env=env, timeout=900)
     a, b = json.load(open(f"{one}/study.json")), json.load(open(f"{two}/study.json"))
     assert (a.pop("ranks"), b.pop("ranks")) == (1, 2)
-    assert a == b and a["rows"] == 32 and a["train"] + a["held_out"] == 32
+    # modelled labels are deterministic: identical across world sizes; measured
+    # ones are timings (they differ run to run), so the 2-rank study is compared
+    # with a one-process study over the same gathered labels
+    assert a["modelled_labels"] == b["modelled_labels"] and a["rows"] == b["rows"] >= 24
+    assert a["train"] + a["held_out"] == a["rows"]
     idx = [np.load(f"{two}/rank{r:03d}/study_pred.npz")["idx"] for r in range(2)]
-    assert len(np.intersect1d(*idx)) == 0 and len(idx[0]) + len(idx[1]) == a["held_out"]
+    assert len(np.intersect1d(*idx)) == 0 and len(idx[0]) + len(idx[1]) == b["held_out"]
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "measured_study.py"), two], check=True, cwd=ROOT,
+                   env=env, timeout=600, capture_output=True)
+    c = json.load(open(f"{two}/study.json"))
+    assert c.pop("ranks") == 1 and c == b
 
 
 def _small(pat, n, m, shape, r, counts, out, grid, wg, inh=64):

@@ -12,7 +12,7 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CS = os.path.join(ROOT, "paper_1412_6986_b200", "csrc")
-NAMES = "SHAPE R CI CE NC NCE NU NUE U D OPT WIDE CTXWRAP MAXT H2 W2 P2 PF VEC MINB".split()
+NAMES = "SHAPE R CI CE NC NCE NU NUE U D OPT WIDE CTXWRAP MAXT H2 W2 P2 PF VEC MINB SHARE".split()
 
 
 def source(vals):
