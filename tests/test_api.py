@@ -88,3 +88,26 @@ def test_emit_optimized_infeasible(golden):
                          5, 1, 0, 0, 0, 0)
     with pytest.raises(L.OptimizationInfeasible):
         L.emit_optimized(L.KernelInstance(p, L.LaunchConfig(2048, 2048, 32, 32)))
+
+
+def test_shared_load_paths_are_exercised_by_the_goldens(golden):
+    """LMT_SHARE (one load per tap for a group of work units with the same
+    home coordinate) is only ever enabled for xy_reuse / x_reuse_* and the
+    golden parity set (run bitwise on the GPU) reaches it for both kinds,
+    in both variants."""
+    seen = {}
+    for r in golden["interp"]:
+        inst = make_instance(r)
+        for variant, src in (("base", L.emit_baseline(inst)), ("opt", None)):
+            if variant == "opt":
+                try:
+                    src = L.emit_optimized(inst)
+                except L.OptimizationInfeasible:
+                    continue
+            d = dict(src.compile_defines)
+            if d["LMT_SHARE"]:
+                assert r["pattern"] in ("xy_reuse", "x_reuse_row", "x_reuse_col"), r
+                assert d["LMT_U"] > 1
+                seen.setdefault((variant, r["pattern"] == "xy_reuse"), 0)
+                seen[(variant, r["pattern"] == "xy_reuse")] += 1
+    assert set(seen) == {("base", True), ("base", False), ("opt", True), ("opt", False)}, seen
