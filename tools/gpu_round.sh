@@ -24,4 +24,4 @@ ncu -i $OUT/prof_top.ncu-rep --page raw --csv > $OUT/raw_top.csv 2>&1
 ncu -i $OUT/prof_top.ncu-rep --page source --csv --print-source sass > $OUT/source_top.csv 2>&1
 gzip -f $OUT/source_top.csv $OUT/raw_top.csv
 mv $OUT/prof_top.ncu-rep /tmp/ 2>/dev/null
-tail -2 $OUT/pytest_gpu.log $OUT/smoke.log $OUT/bench.err; cat $OUT/fp32_peak.json $OUT/bench.json
+for f in $OUT/pytest_gpu.log $OUT/smoke.log $OUT/bench.err; do tail -n 2 $f; done; cat $OUT/fp32_peak.json $OUT/bench.json
