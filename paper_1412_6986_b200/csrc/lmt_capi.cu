@@ -478,7 +478,9 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
             const int64_t slot = sets(U) * K + p.num_coal_ilb + p.num_uncoal_ilb;
             const int64_t regs = std::min<int64_t>(jit_regs_guess(K, slot, U, 2), 65536 / maxt);
             const int64_t rregs = (regs + 7) / 8 * 8;
-            for (int Sx : {2 * U, U}) {
+            const bool sh = jit_share(A, U);
+            for (int Sx : {2 * U, U + 1, U}) {
+                if (Sx == U + 1 && (!sh || U == 1)) continue;
                 const int64_t S = std::min<int64_t>({(int64_t)Sx, kMaxStagesJ, std::max<int64_t>(nit, 1)});
                 if (S < U || S * stage_bytes > smem_cap) continue;
                 int64_t res = std::min<int64_t>(32, 64 / std::max<int64_t>(1, warps));
@@ -487,7 +489,8 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
                 res = std::max<int64_t>(res, 1);
                 const int64_t act = std::min<int64_t>(res, (ctas + sms - 1) / sms);
                 const double chains = std::min(64.0, (double)act * (double)warps * U / 4.0);
-                const bool overlap = S >= 2 * U;
+                // shared loads release U - 1 slots early (lmt_jit.cuh), so U + 1 slots overlap too
+                const bool overlap = S >= 2 * U || (sh && S >= U + 1);
                 const double score = chains * 64.0 + (overlap ? 16.0 : 0.0) + U * 2.0;
                 if (score > best) { best = score; bu = U; bs = (int)S; }
             }

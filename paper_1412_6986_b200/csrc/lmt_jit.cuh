@@ -123,6 +123,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
         : "memory");
 }
 
+// non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(unsigned long long *bar, unsigned parity) {
+    unsigned r;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(r)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return r != 0;
+}
+
 // L1 prefetch: no destination register, so no scoreboard for the step
 // that consumes the line later to wait on.
 __device__ __forceinline__ void prefetch_l1(const float *p) {
@@ -525,13 +538,30 @@ __device__ __forceinline__ int region_shift(const SynthArgs &A, int it) {
     return (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & 3;
 }
 
-// Slots: iteration `it` lives in slot it % S; thread 0 re-arms a slot for
-// iteration it + S once every warp released it. With S >= 2U a group's
-// regions are in flight while the previous group computes.
+// A warp is done with the slot of iteration `it`: arrive on its empty
+// barrier; whichever warp then sees the phase complete (the last to arrive,
+// or one that checks after it) and wins the claim re-arms the slot with
+// iteration it + S. No warp waits for another to reach a group boundary.
+__device__ __forceinline__ void release_slot(const SynthArgs &A, const TensorMap *map, float *smem,
+                                             unsigned long long *full, unsigned long long *empty, int *claim, int it,
+                                             int S, int nit) {
+    const int s = it % S;
+    mbar_arrive(&empty[s]);
+    if (it + S < nit && mbar_test(&empty[s], (it / S) & 1) && atomicCAS(&claim[s], it, it + S) == it)
+        stage_region(A, map, smem, full, s, it + S);
+}
+
+// Slots: iteration `it` lives in slot it % S and is re-armed for it + S as
+// soon as every warp released it (release_slot). With S >= 2U a group's
+// regions are in flight while the previous group computes. With LMT_SHARE
+// the group's U regions are identical: every unit reads the last unit's
+// slot and the other U - 1 are released as soon as they have landed, so
+// S >= U + 1 already overlaps the next group's staging with this group.
 extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
     lmt_kernel(const __grid_constant__ TensorMap tmap, const SynthArgs A) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) unsigned long long full[kMaxStagesJ], empty[kMaxStagesJ];
+    __shared__ int claim[kMaxStagesJ];  // iteration slot s holds / was last armed for
 
     const int wi_x = threadIdx.x, wi_y = threadIdx.y;
     const int wg_w = blockDim.x, wg_h = blockDim.y;
@@ -545,6 +575,7 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], nwarps);
+            claim[s] = s;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -564,18 +595,8 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
     const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
     const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
 
-    int prev0 = 0, prevcnt = 0;
     for (int it0 = 0; it0 < nit;) {
         const int cnt = (it0 + U <= nit) ? U : 1;
-        if (tid == 0) {  // re-arm the slots the previous group released
-            for (int q = 0; q < prevcnt; ++q) {
-                const int pit = prev0 + q;
-                if (pit + S < nit) {
-                    mbar_wait(&empty[pit % S], (pit / S) & 1);
-                    stage_region(A, &tmap, smem, full, pit % S, pit + S);
-                }
-            }
-        }
         if (cnt == U) {
 #if LMT_WIDE
             SmemWideSrc src;
@@ -587,8 +608,8 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
             size_t o[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int it = it0 + u;
-                mbar_wait(&full[it % S], (it / S) & 1);
+                const int it = SHARE ? it0 + U - 1 : it0 + u;  // the slot this unit reads
+                mbar_wait(&full[(it0 + u) % S], ((it0 + u) / S) & 1);
                 const float *slot = smem + (it % S) * A.stage_floats;
 #if LMT_WIDE
                 src.slot[u] = slot;
@@ -597,8 +618,14 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
 #else
                 src.p[u] = slot + region_shift(A, it) + (hr0 * A.bw + hc0);
 #endif
-                const int ix = it % A.nwx, iy = it / A.nwx;
+                const int ix = (it0 + u) % A.nwx, iy = (it0 + u) / A.nwx;
                 o[u] = (size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w);
+            }
+            if (SHARE) {  // the U - 1 regions nobody reads go back to the producer now
+                __syncwarp();
+                if (lane == 0)
+                    for (int q = 0; q < U - 1; ++q)
+                        release_slot(A, &tmap, smem, full, empty, claim, it0 + q, S, nit);
             }
             float acc[U];
             run_units<U>(A, src, in2c, in2u, acc);
@@ -625,10 +652,10 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
             A.out[(size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w)] = acc[0];
         }
         __syncwarp();
-        if (lane == 0)
-            for (int q = 0; q < cnt; ++q) mbar_arrive(&empty[(it0 + q) % S]);
-        prev0 = it0;
-        prevcnt = cnt;
+        if (lane == 0) {
+            const int q0 = (SHARE && cnt == U) ? U - 1 : 0;
+            for (int q = q0; q < cnt; ++q) release_slot(A, &tmap, smem, full, empty, claim, it0 + q, S, nit);
+        }
         it0 += cnt;
     }
 }
