@@ -252,6 +252,12 @@ struct DevCtx {
     size_t dres_cap = 0;        // instances
     std::vector<cudaEvent_t> events;
     bool attrs_set = false;
+    // host-buffer measurement: two slots of device inputs/outputs so the
+    // copies of instance i +- 1 (own streams) overlap the kernels of instance i
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t copied[2] = {}, consumed[2] = {}, drained[2] = {};
+    float *hin[2] = {}, *hin2[2] = {}, *hob[2] = {}, *hoo[2] = {};
+    size_t hin_cap[2] = {}, hin2_cap[2] = {}, hob_cap[2] = {}, hoo_cap[2] = {};
 };
 
 std::mutex g_mu;
@@ -268,6 +274,15 @@ int get_ctx(DevCtx **out) {
         CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         c.smem_optin = (size_t)optin;
         CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; b++) {
+            CUDA_TRY(cudaEventCreateWithFlags(&c.copied[b], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c.consumed[b], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c.drained[b], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(c.consumed[b], c.stream));  // complete: nothing in flight yet
+            CUDA_TRY(cudaEventRecord(c.drained[b], c.stream));
+        }
         c.device = dev;
     }
     if (!g_encode) {
@@ -956,61 +971,105 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         const size_t need_in = (size_t)(rows * pitch) * pl.in_copies + 64, need_out = (size_t)p.out_h * p.out_w;
         const size_t need_in2 = in2_phys_elems(p.in_h, p.in_w);
         const int64_t p2 = in2_pitch(p.in_w);
-        if (host || c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in ||
-            c->in_copies < pl.in_copies) {
-            if (need_in > c->in_cap) {
+        float *din, *din2, *dob, *doo;
+        const int b = (int)(i & 1);
+        if (host) {
+            // slot b was last used by instance i - 2: its buffers grow only with every stream idle
+            if (need_in > c->hin_cap[b] || need_in2 > c->hin2_cap[b] || need_out > c->hob_cap[b] ||
+                need_out > c->hoo_cap[b]) {
                 CUDA_TRY(cudaStreamSynchronize(s));
-                size_t fr = 0, tot = 0;
-                CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-                if (need_in * 4 + ((size_t)256 << 20) > fr + c->in_cap * 4) {
-                    m.status = fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i, need_in * 4);
-                    continue;
+                CUDA_TRY(cudaStreamSynchronize(c->h2d));
+                CUDA_TRY(cudaStreamSynchronize(c->d2h));
+                if (need_in > c->hin_cap[b]) {
+                    size_t fr = 0, tot = 0;
+                    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+                    if (need_in * 4 + ((size_t)256 << 20) > fr + c->hin_cap[b] * 4) {
+                        m.status = fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i,
+                                        need_in * 4);
+                        continue;
+                    }
                 }
-                rc = ensure(&c->in, &c->in_cap, need_in);
-                if (rc) return rc;
+                if ((rc = ensure(&c->hin[b], &c->hin_cap[b], need_in)) ||
+                    (rc = ensure(&c->hin2[b], &c->hin2_cap[b], need_in2)) ||
+                    (rc = ensure(&c->hob[b], &c->hob_cap[b], need_out)) ||
+                    (rc = ensure(&c->hoo[b], &c->hoo_cap[b], need_out)))
+                    return rc;
             }
+            din = c->hin[b];
+            din2 = c->hin2[b];
+            dob = c->hob[b];
+            doo = c->hoo[b];
+            // H2D on its own stream once instance i - 2's kernels are done with the slot
+            CUDA_TRY(cudaStreamWaitEvent(c->h2d, c->consumed[b], 0));
+            CUDA_TRY(cudaMemcpy2DAsync(din, (size_t)pitch * 4, h_in[i], (size_t)cols * 4, (size_t)cols * 4,
+                                       (size_t)rows, cudaMemcpyHostToDevice, c->h2d));
+            CUDA_TRY(cudaMemcpy2DAsync(din2, (size_t)p2 * 4, h_in2[i], (size_t)p.in_w * 4, (size_t)p.in_w * 4,
+                                       (size_t)p.in_h, cudaMemcpyHostToDevice, c->h2d));
+            CUDA_TRY(cudaEventRecord(c->copied[b], c->h2d));
+            CUDA_TRY(cudaStreamWaitEvent(s, c->copied[b], 0));
             CUDA_TRY(cudaEventRecord(ev[3], s));
-            if (host) {
-                CUDA_TRY(cudaMemcpy2DAsync(c->in, (size_t)pitch * 4, h_in[i], (size_t)cols * 4, (size_t)cols * 4,
-                                           (size_t)rows, cudaMemcpyHostToDevice, s));
-            } else {
-                rc = launch_fill(c->in, rows, cols, pitch, 0, s, c->sms);
-                if (rc) return rc;
-            }
-            m.launches += host ? 0 : 1;
+            filled[(size_t)i] = 1;
             if (pl.in_copies > 1) {
-                rc = launch_in_shift(c->in, rows, pitch, s, c->sms);
+                rc = launch_in_shift(din, rows, pitch, s, c->sms);
                 if (rc) return rc;
                 m.launches += 1;
             }
-            c->in_copies = pl.in_copies;
-            c->in_rows = host ? -1 : rows;
-            c->in_cols = host ? -1 : cols;
-            c->in_pitch = host ? -1 : pitch;
-            filled[(size_t)i] = 1;
-        }
-        if (host || c->in2_h != p.in_h || c->in2_w != p.in_w || !c->in2) {
-            rc = ensure(&c->in2, &c->in2_cap, need_in2);
+            rc = launch_in2_halo(din2, p.in_h, p.in_w, s, c->sms);
             if (rc) return rc;
-            if (!filled[(size_t)i]) { CUDA_TRY(cudaEventRecord(ev[3], s)); filled[(size_t)i] = 1; }
-            if (host) {
-                CUDA_TRY(cudaMemcpy2DAsync(c->in2, (size_t)p2 * 4, h_in2[i], (size_t)p.in_w * 4, (size_t)p.in_w * 4,
-                                           (size_t)p.in_h, cudaMemcpyHostToDevice, s));
-            } else {
+            m.launches += 1;
+            // the outputs of slot b must have reached the host (instance i - 2)
+            CUDA_TRY(cudaStreamWaitEvent(s, c->drained[b], 0));
+        } else {
+            if (c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in ||
+                c->in_copies < pl.in_copies) {
+                if (need_in > c->in_cap) {
+                    CUDA_TRY(cudaStreamSynchronize(s));
+                    size_t fr = 0, tot = 0;
+                    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+                    if (need_in * 4 + ((size_t)256 << 20) > fr + c->in_cap * 4) {
+                        m.status = fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i, need_in * 4);
+                        continue;
+                    }
+                    rc = ensure(&c->in, &c->in_cap, need_in);
+                    if (rc) return rc;
+                }
+                CUDA_TRY(cudaEventRecord(ev[3], s));
+                rc = launch_fill(c->in, rows, cols, pitch, 0, s, c->sms);
+                if (rc) return rc;
+                m.launches += 1;
+                if (pl.in_copies > 1) {
+                    rc = launch_in_shift(c->in, rows, pitch, s, c->sms);
+                    if (rc) return rc;
+                    m.launches += 1;
+                }
+                c->in_copies = pl.in_copies;
+                c->in_rows = rows;
+                c->in_cols = cols;
+                c->in_pitch = pitch;
+                filled[(size_t)i] = 1;
+            }
+            if (c->in2_h != p.in_h || c->in2_w != p.in_w || !c->in2) {
+                rc = ensure(&c->in2, &c->in2_cap, need_in2);
+                if (rc) return rc;
+                if (!filled[(size_t)i]) { CUDA_TRY(cudaEventRecord(ev[3], s)); filled[(size_t)i] = 1; }
                 rc = launch_fill(c->in2, p.in_h, p.in_w, p2, 1, s, c->sms);
                 if (rc) return rc;
                 m.launches += 1;
+                rc = launch_in2_halo(c->in2, p.in_h, p.in_w, s, c->sms);
+                if (rc) return rc;
+                m.launches += 1;
+                c->in2_h = p.in_h;
+                c->in2_w = p.in_w;
             }
-            rc = launch_in2_halo(c->in2, p.in_h, p.in_w, s, c->sms);
+            rc = ensure(&c->outb, &c->outb_cap, need_out);
             if (rc) return rc;
-            m.launches += 1;
-            c->in2_h = host ? -1 : p.in_h;
-            c->in2_w = host ? -1 : p.in_w;
+            rc = ensure(&c->outo, &c->outo_cap, need_out);
+            if (rc) return rc;
+            din = c->in;
+            din2 = c->in2;
+            dob = c->outb;
+            doo = c->outo;
         }
-        rc = ensure(&c->outb, &c->outb_cap, need_out);
-        if (rc) return rc;
-        rc = ensure(&c->outo, &c->outo_cap, need_out);
-        if (rc) return rc;
         // ---- K1, K2 timed with events on the launching stream; a kernel not
         // yet compiled/loaded is resolved first, outside the events
         if (pl.jit) {
@@ -1023,7 +1082,7 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
             m.kernel_id = jit_kid(gb, go);  // the kernels built
         }
         CUDA_TRY(cudaEventRecord(ev[0], s));
-        rc = launch_variant(pl, 0, c->in, rows, cols, pitch, c->in2, c->outb, s);
+        rc = launch_variant(pl, 0, din, rows, cols, pitch, din2, dob, s);
         if (rc) { m.status = rc; continue; }
         CUDA_TRY(cudaEventRecord(ev[1], s));
         ran_base[(size_t)i] = 1;
@@ -1033,7 +1092,7 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
                              (pl.feasible || ((flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
                                               (int64_t)pl.A.stage_bytes <= (int64_t)c->smem_optin - 1024));
         if (run_opt) {
-            rc = launch_variant(pl, 1, c->in, rows, cols, pitch, c->in2, c->outo, s);
+            rc = launch_variant(pl, 1, din, rows, cols, pitch, din2, doo, s);
             if (rc) { m.status = rc; continue; }
             CUDA_TRY(cudaEventRecord(ev[2], s));
             ran_opt[(size_t)i] = 1;
@@ -1041,14 +1100,20 @@ static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *
         } else if (!pl.feasible) {
             m.status = LMT_ERR_INFEASIBLE;
         }
-        rc = launch_digest(c->outb, run_opt ? c->outo : nullptr, (int64_t)need_out, c->dres + i * 3, s, c->sms);
+        rc = launch_digest(dob, run_opt ? doo : nullptr, (int64_t)need_out, c->dres + i * 3, s, c->sms);
         if (rc) return rc;
         m.launches += 1;
-        if (host && h_ob && h_ob[i])
-            CUDA_TRY(cudaMemcpyAsync(h_ob[i], c->outb, need_out * 4, cudaMemcpyDeviceToHost, s));
-        if (host && run_opt && h_oo && h_oo[i])
-            CUDA_TRY(cudaMemcpyAsync(h_oo[i], c->outo, need_out * 4, cudaMemcpyDeviceToHost, s));
+        if (host) {  // D2H on its own stream, overlapping instance i + 1
+            CUDA_TRY(cudaEventRecord(c->consumed[b], s));
+            CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->consumed[b], 0));
+            if (h_ob && h_ob[i])
+                CUDA_TRY(cudaMemcpyAsync(h_ob[i], dob, need_out * 4, cudaMemcpyDeviceToHost, c->d2h));
+            if (run_opt && h_oo && h_oo[i])
+                CUDA_TRY(cudaMemcpyAsync(h_oo[i], doo, need_out * 4, cudaMemcpyDeviceToHost, c->d2h));
+            CUDA_TRY(cudaEventRecord(c->drained[b], c->d2h));
+        }
     }
+    if (host) CUDA_TRY(cudaStreamSynchronize(c->d2h));
     std::vector<unsigned long long> res((size_t)std::max<int64_t>(n, 1) * 3);
     CUDA_TRY(cudaMemcpyAsync(res.data(), c->dres, res.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));

@@ -30,9 +30,10 @@ def study_set(table, labels: np.ndarray):
     """Rows of a gathered label matrix (run_sweep: row, t_base_ms, t_opt_ms,
     mismatches, status) that enter the study: measured without failure (the
     optimized variant may be infeasible: label 0.0, cost_model.py:154-157),
-    no output mismatch, features valid. Returns (rows, X, modelled, measured)
-    in row order."""
+    no output mismatch, a dataset row (not invalid / unsupported). Returns
+    (rows, X, modelled, measured) in row order."""
     from .access_analysis import features_records
+    from .dataset import STATUS_INVALID, STATUS_UNSUPPORTED
 
     lab = labels[np.argsort(labels[:, 0], kind="stable")]
     rows = lab[:, 0].astype(np.int64)
@@ -42,7 +43,7 @@ def study_set(table, labels: np.ndarray):
     rows, tb, to = rows[keep], tb[keep], to[keep]
     measured = np.where(to > 0, tb / np.where(to > 0, to, 1.0), 0.0)
     fb = features_records(table.records(rows))
-    ok = fb.status == 0
+    ok = (fb.status != STATUS_INVALID) & (fb.status != STATUS_UNSUPPORTED)  # DatasetArrays.ok: infeasible stays (0.0)
     return rows[ok], fb.X[ok], fb.label[ok], measured[ok]
 
 

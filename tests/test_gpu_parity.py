@@ -55,6 +55,25 @@ def test_run_pair_matches_reference_all_cases(golden):
     assert not bad, bad
 
 
+def test_measure_host_buffers_match_reference(golden):
+    """lmt_measure_batch_host (the e2e path: host inputs, double-buffered
+    device slots, copies on their own streams): per-instance outputs read
+    back bit-identical to the reference's, digests equal to the device-input
+    path's, across more instances than slots and with growing sizes."""
+    recs = golden["interp"][:12]
+    insts = [make_instance(r) for r in recs]
+    ins = [L.make_inputs(k) for k in insts]
+    ob = [np.full((k.params.out_h, k.params.out_w), np.nan, np.float32) for k in insts]
+    oo = [np.full_like(o, np.nan) for o in ob]
+    got = L.measure_instances_host(insts, [a for a, _ in ins], [b for _, b in ins], out_base=ob, out_opt=oo)
+    dev = L.measure_instances(insts)
+    for r, m, d, b, o in zip(recs, got, dev, ob, oo):
+        assert m.status in (0, 2) and m.digest_base == d.digest_base
+        assert oracle.out_hash(b) == int(r["digest"])
+        if m.t_opt_ms is not None:
+            assert m.mismatches == 0 and np.array_equal(b, o) and m.digest_opt == d.digest_opt
+
+
 def test_inf_cases_present_and_exact(golden):
     inf_cases = [r for r in golden["interp"] if r["n_inf"] > 0]
     assert inf_cases, "golden set must include +-inf producing chains"
