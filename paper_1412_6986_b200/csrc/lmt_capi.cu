@@ -1165,18 +1165,44 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
         if (rc) return rc;
         device = c->device;
         const lmt_device d = dev_or_default(dev);
+        size_t fr = 0, tot = 0;
+        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+        size_t max_in = 0, max_in2 = 0, max_out = 0;
         for (int64_t i = 0; i < n; i++) {
             const lmt_instance &p = insts[i];
             if (!violations(p).empty()) continue;
             lmt_geometry g0;
             if (compute_geometry(p, d, &g0)) continue;
             Plan pl;
-            if (make_plan(p, d, round_up(g0.alloc_w, 4), &pl, c) || !pl.jit) continue;
+            if (make_plan(p, d, round_up(g0.alloc_w, 4), &pl, c)) continue;
+            // the device-input buffers the batch will need (measure_impl's sizes)
+            const size_t need_in = (size_t)(g0.alloc_h * round_up(g0.alloc_w, 4)) * pl.in_copies + 64;
+            if (need_in * 4 + ((size_t)1 << 30) <= fr + c->in_cap * 4) max_in = std::max(max_in, need_in);
+            max_in2 = std::max(max_in2, in2_phys_elems(p.in_h, p.in_w));
+            max_out = std::max(max_out, (size_t)p.out_h * p.out_w);
+            if (!pl.jit) continue;
             keys.push_back(pl.kb);
             const bool run_opt = !(flags & LMT_MEASURE_SKIP_OPT) &&
                                  (pl.feasible || ((flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
                                                   (int64_t)pl.A.stage_bytes <= (int64_t)c->smem_optin - 1024));
             if (run_opt) keys.push_back(pl.ko);
+        }
+        // reserve them now: growing a buffer inside a timed batch means a
+        // stream sync and a multi-GB cudaFree/cudaMalloc with the GPU idle
+        if (max_in > c->in_cap) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            if ((rc = ensure(&c->in, &c->in_cap, max_in))) return rc;
+            c->in_rows = c->in_cols = c->in_pitch = -1;  // contents no longer valid
+        }
+        if (max_in2 > c->in2_cap) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            if ((rc = ensure(&c->in2, &c->in2_cap, max_in2))) return rc;
+            c->in2_h = c->in2_w = -1;
+        }
+        if (max_out > c->outb_cap || max_out > c->outo_cap) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            if ((rc = ensure(&c->outb, &c->outb_cap, max_out)) || (rc = ensure(&c->outo, &c->outo_cap, max_out)))
+                return rc;
         }
     }
     std::sort(keys.begin(), keys.end());
