@@ -192,10 +192,19 @@ __global__ void k_mvt1_opt(const float *__restrict__ A, const float *__restrict_
     float *sA = s, *sy = s + wg * P;
     const int i0 = blockIdx.x * wg, ti = threadIdx.x;
     float acc = x1_0[i0 + ti];
+    // wg a multiple of T (every instance of real.instance_set): thread ti
+    // copies column ti % T of rows ti / T, ti / T + wg / T, ... -- the same
+    // elements as the generic walk, without a division per element
+    const bool even = wg % T == 0;
+    const int r0 = ti / T, c0 = ti - r0 * T, rstep = wg / T;
     for (int j0 = 0; j0 < n; j0 += T) {
-        for (int e = ti; e < wg * T; e += wg) {
-            const int r = e / T, cc = e - r * T;
-            sA[r * P + cc] = A[(size_t)(i0 + r) * n + j0 + cc];
+        if (even) {
+            for (int r = r0; r < wg; r += rstep) sA[r * P + c0] = A[(size_t)(i0 + r) * n + j0 + c0];
+        } else {
+            for (int e = ti; e < wg * T; e += wg) {
+                const int r = e / T, cc = e - r * T;
+                sA[r * P + cc] = A[(size_t)(i0 + r) * n + j0 + cc];
+            }
         }
         for (int e = ti; e < T; e += wg) sy[e] = y1[j0 + e];
         __syncthreads();
