@@ -87,14 +87,43 @@ typedef struct lmt_measurement {
     int32_t kernel_id;       /* which specialised kernel ran (diagnostics) */
     int32_t launches;        /* kernels this instance launched (fill, K1, K2, digest) */
     int32_t nstages;         /* shared-memory stages the optimized variant used */
+    int32_t lane_sms;        /* SMs of the partition it ran in; 0 = the whole device (isolated) */
+    int32_t order;           /* 0: baseline timed first, 1: optimized timed first */
+    int32_t in_copies;       /* 4: the baseline read 128-bit shifted copies of `in`; building them is
+                                inside t_base_ms. 1: plain `in` */
+    int32_t ctas;            /* CTAs (workgroups) per launch */
 } lmt_measurement;
 
 typedef struct lmt_forest lmt_forest;
 
-/* flags for lmt_measure_batch */
-#define LMT_MEASURE_SKIP_OPT     0x1  /* run the baseline only */
-#define LMT_MEASURE_KEEP_OUTPUTS 0x2  /* leave the last instance's outs readable via lmt_last_outputs */
-#define LMT_MEASURE_ALLOW_LARGE_LMEM 0x4 /* run the optimized variant past the device lmem cap (B200 has 227 KB) */
+/* flags for lmt_measure_batch*
+ *
+ * Measurement contract: each variant is timed alone on
+ * its SMs with CUDA events on its launching stream; the variant order
+ * alternates between instances (odd instances time the optimized variant
+ * first). On the whole device the L2 is flushed before each variant (a
+ * 192 MB scrub outside the events), so both variants start L2-cold. With
+ * LMT_MEASURE_CONCURRENT, instances whose launch has at most as many CTAs as
+ * the largest SM partition run inside disjoint SM partitions (green
+ * contexts), several at once; a CTA still gets an SM of its own, as on the
+ * whole device, and these long launches are not flushed (a flush would evict
+ * the neighbouring partitions' working sets too). */
+#define LMT_MEASURE_SKIP_OPT         0x1  /* run the baseline only */
+#define LMT_MEASURE_ALLOW_LARGE_LMEM 0x4  /* run the optimized variant past the device lmem cap (B200 has 227 KB) */
+#define LMT_MEASURE_CONCURRENT       0x8  /* few-CTA launches run concurrently in disjoint SM partitions */
+#define LMT_MEASURE_REGBLOCK         0x10 /* register-blocked variants: the work units of a thread whose home
+                                             coordinates coincide share their stencil loads (and, optimized,
+                                             their staged region); default: every work unit issues its own
+                                             loads, like the emitted kernel (codegen.py:268-283) */
+#define LMT_MEASURE_WARM_L2          0x20 /* no L2 flush before the isolated variants */
+
+/* Options of lmt_measure_batch_ex. */
+typedef struct lmt_measure_opts {
+    int32_t flags;
+    int32_t samples;            /* output cells gathered per instance (0: none) */
+    const int64_t *sample_idx;  /* [n][samples] linear indices into out (row * out_w + col) */
+    float *h_sample_vals;       /* [n][samples][2]: baseline, optimized value (0 when not run) */
+} lmt_measure_opts;
 
 const char *lmt_version(void);
 const char *lmt_last_error(void);
@@ -114,9 +143,11 @@ int lmt_fill(float *d_dst, int64_t rows, int64_t cols, int64_t pitch, uint32_t s
 
 /* interp.execute (interp.py:41-114) on the GPU. variant 0 = BASELINE
  * (plain global loads), 1 = OPTIMIZED (region staged in shared memory by
- * TMA). d_in is [in_rows, in_cols] with row pitch in_pitch floats (a multiple
- * of 4, 16-byte aligned base); d_in2 is [in_h, in_w]; d_out [out_h, out_w].
- * Asynchronous on `stream`. */
+ * TMA). d_in is [in_rows, in_cols] with row pitch in_pitch floats (in_pitch
+ * >= in_cols, a multiple of 4, 16-byte aligned base); d_in2 is [in_h, in_w];
+ * d_out [out_h, out_w]. Asynchronous on `stream`; d_in is read as is (no
+ * copy), in2 is staged into the kernels' wrapped-halo layout in stream-
+ * ordered scratch. */
 int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant,
                 const float *d_in, int64_t in_rows, int64_t in_cols, int64_t in_pitch,
                 const float *d_in2, float *d_out, void *stream);
@@ -139,6 +170,20 @@ int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_devic
                            const int64_t *in_cols, const float *const *h_in2,
                            float *const *h_out_base, float *const *h_out_opt,
                            lmt_measurement *out);
+
+/* Both of the above, plus sampled output cells for an independent check
+ * (the CPU oracle) of every measured instance. h_in == NULL: device-generated
+ * inputs (lmt_measure_batch); otherwise host buffers (lmt_measure_batch_host). */
+int lmt_measure_batch_ex(const lmt_instance *insts, int64_t n, const lmt_device *dev,
+                         const lmt_measure_opts *opts, const float *const *h_in, const int64_t *in_rows,
+                         const int64_t *in_cols, const float *const *h_in2, float *const *h_out_base,
+                         float *const *h_out_opt, lmt_measurement *out);
+
+/* The SM partitions LMT_MEASURE_CONCURRENT runs in on the current device:
+ * their sizes in SMs (largest first) into sizes[cap]; *count = partitions
+ * (0 when the driver offers no green contexts: every instance then runs on
+ * the whole device). */
+int lmt_partitions(int32_t *sizes, int32_t cap, int32_t *count);
 
 /* Order-independent 64-bit digest of an fp32 device array (the digest in
  * lmt_measurement). */
@@ -220,10 +265,11 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
 
 /* The CUDA source the specialised kernel of (instance, variant) is compiled
  * from -- its #defines then the kernel text -- the counterpart of
- * codegen.emit_baseline / emit_optimized (codegen.py:336-354). *len_out =
- * bytes needed (without the NUL); buf may be NULL to query. */
-int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, char *buf, int64_t cap,
-                      int64_t *len_out);
+ * codegen.emit_baseline / emit_optimized (codegen.py:336-354). flags: the
+ * lmt_measure_batch flags that shape the kernel (LMT_MEASURE_REGBLOCK).
+ * *len_out = bytes needed (without the NUL); buf may be NULL to query. */
+int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, int32_t flags, char *buf,
+                      int64_t cap, int64_t *len_out);
 
 /* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
  * compiles) and the host seconds spent compiling. */

@@ -187,9 +187,12 @@ typedef struct exec_ctx {
     int64_t wg_begin, wg_end;
     int64_t next;           /* shared work counter (under lock) */
     int64_t budget;         /* > 0: stop after this many work units (timing samples) */
+    int64_t wg_units;       /* > 0: stop each workgroup after this many work units */
     pthread_mutex_t lock;
     int err;
 } exec_ctx;
+
+static _Thread_local int64_t g_prefix_units = 0;  /* ora_execute_prefix -> ora_execute */
 
 /* One workgroup, following interp.py:62-113 statement by statement. */
 static int run_workgroup(exec_ctx *x, int64_t gy, int64_t gx, float *region, float *acc) {
@@ -200,6 +203,7 @@ static int run_workgroup(exec_ctx *x, int64_t gy, int64_t gx, float *region, flo
     const int64_t in2_h = p->in_h, in2_w = p->in_w;
     const int64_t pad = g->pad;
     const int64_t rcp = g->r_cols_pad;
+    int64_t units = 0;
     for (int64_t it_y = 0; it_y < nwy; it_y++) {
         for (int64_t it_x = 0; it_x < nwx; it_x++) {
             const int64_t wu_x0 = gx * (wg_w * nwx) + it_x * wg_w;
@@ -227,6 +231,7 @@ static int run_workgroup(exec_ctx *x, int64_t gy, int64_t gx, float *region, flo
             for (int64_t lane = 0; lane < wg_size; lane++) acc[lane] = 0.0f;
             for (int64_t lane = 0; lane < wg_size; lane++) {
                 if (x->budget > 0 && --x->budget == 0) return ORA_OK;
+                if (x->wg_units > 0 && units++ == x->wg_units) return ORA_OK;
                 const int64_t wi_x = lane % wg_w, wi_y = lane / wg_w;
                 const int64_t glin = (gy * wg_h + wi_y) * p->grid_x + (gx * wg_w + wi_x);
                 const int64_t wu_x = wu_x0 + wi_x, wu_y = wu_y0 + wi_y;
@@ -328,6 +333,7 @@ int ora_execute(const ora_instance *p, const ora_device *dev, int variant,
     x->in_cols = in_cols;
     x->in2 = in2;
     x->out = out;
+    x->wg_units = g_prefix_units;
     x->K = ora_stencil_offsets(p->stencil_shape, p->stencil_radius, x->dr, x->dc, 1024);
     const int64_t nwg = (int64_t)(p->grid_x / p->wg_x) * (p->grid_y / p->wg_y);
     x->wg_begin = wg_begin < 0 ? 0 : wg_begin;
@@ -342,6 +348,19 @@ int ora_execute(const ora_instance *p, const ora_device *dev, int variant,
     rc = x->err;
     pthread_mutex_destroy(&x->lock);
     free(x);
+    return rc;
+}
+
+/* ora_execute over workgroups [wg_begin, wg_end) with each workgroup cut
+ * after `units_per_wg` work units (in its own iteration/lane order): a
+ * bounded multi-core timing sample of the reference's CPU path that still
+ * runs whole-workgroup code on every thread (bench.py's reference arm). */
+int ora_execute_prefix(const ora_instance *p, const ora_device *dev, int variant, const float *in, int64_t in_rows,
+                       int64_t in_cols, const float *in2, float *out, int nthreads, int64_t wg_begin, int64_t wg_end,
+                       int64_t units_per_wg) {
+    g_prefix_units = units_per_wg;
+    int rc = ora_execute(p, dev, variant, in, in_rows, in_cols, in2, out, nthreads, wg_begin, wg_end);
+    g_prefix_units = 0;
     return rc;
 }
 
@@ -506,6 +525,7 @@ int64_t ora_execute_sample(const ora_instance *p, const ora_device *dev, int var
     x->in_cols = in_cols;
     x->in2 = in2;
     x->out = out;
+    x->wg_units = g_prefix_units;
     x->K = ora_stencil_offsets(p->stencil_shape, p->stencil_radius, x->dr, x->dc, 1024);
     x->budget = max_units + 1;
     const int64_t wg_size = (int64_t)p->wg_x * p->wg_y;
@@ -517,4 +537,139 @@ int64_t ora_execute_sample(const ora_instance *p, const ora_device *dev, int var
     free(acc);
     free(x);
     return rc == ORA_OK ? done : -1;
+}
+
+/* ---------------------------------------------------------------------------
+ * Point evaluation of selected work units with make_inputs' arrays computed
+ * on the fly: in[r][c] = hash(r * alloc_w + c, salt 0), in2[r][c] =
+ * hash(r * in_w + c, salt 1) (interp.py:22-38). Nothing is materialised, so
+ * a paper-size instance (`in` up to ~1 GiB) checks in microseconds per unit.
+ * The arithmetic is run_workgroup's (interp.py:83-113) for the one workitem
+ * and iteration that own the unit (kernel_model.py:158-170). Variant 1 also
+ * checks that the unit's region copy and every region read stay in bounds
+ * (interp.py:71-82, 94-97); given that, its value is the baseline's.
+ * --------------------------------------------------------------------------- */
+static float hash_at(int64_t i, uint32_t salt) {
+    uint32_t v = (uint32_t)((uint64_t)(i + (int64_t)salt) * 2654435761ull);
+    return (float)((double)v / 4294967296.0 - 0.5);
+}
+
+typedef struct eval_ctx {
+    const ora_instance *p;
+    ora_geometry g;
+    int variant;
+    const int64_t *idx;
+    int64_t count;
+    float *vals;
+    int32_t dr[1024], dc[1024];
+    int K;
+    int tid, nthreads;
+    int err;
+} eval_ctx;
+
+static int eval_one(const eval_ctx *x, int64_t unit, float *val) {
+    const ora_instance *p = x->p;
+    const ora_geometry *g = &x->g;
+    const int64_t wg_w = p->wg_x, wg_h = p->wg_y;
+    const int64_t nwx = p->out_w / p->grid_x, nwy = p->out_h / p->grid_y;
+    const int64_t wu_y = unit / p->out_w, wu_x = unit % p->out_w;
+    /* kernel_model.py:158-170 inverted: blocked across groups, cyclic across items */
+    const int64_t gx = wu_x / (wg_w * nwx), rx = wu_x % (wg_w * nwx);
+    const int64_t gy = wu_y / (wg_h * nwy), ry = wu_y % (wg_h * nwy);
+    const int64_t wi_x = rx % wg_w, wi_y = ry % wg_h;
+    const int64_t wu_x0 = wu_x - wi_x, wu_y0 = wu_y - wi_y;
+    const int64_t glin = (gy * wg_h + wi_y) * p->grid_x + (gx * wg_w + wi_x);
+    const int64_t pad = g->pad, aw = g->alloc_w, ah = g->alloc_h;
+    const int64_t in2_h = p->in_h, in2_w = p->in_w;
+    int64_t org_row = 0, org_col = 0;
+    if (x->variant == 1) {
+        org_row = g->org_row_wu_x * wu_x0 + g->org_row_wu_y * wu_y0 + g->off_min_row;
+        org_col = g->org_col_wu_x * wu_x0 + g->org_col_wu_y * wu_y0 + g->off_min_col;
+        /* the whole padded region is copied (interp.py:75-82) */
+        if (org_row + pad < 0 || org_row + pad + g->r_rows > ah || org_col + pad < 0 ||
+            org_col + pad + g->r_cols_pad > aw)
+            return ORA_ERR_BOUNDS;
+    }
+    float a = 0.0f;
+    for (int64_t i = 0; i < p->n; i++) {
+        for (int64_t j = 0; j < p->m; j++) {
+            const int64_t idx_o = g->org_row_wu_x * wu_x + g->org_row_wu_y * wu_y + g->row_i * i + g->row_j * j;
+            const int64_t idx_i = g->org_col_wu_x * wu_x + g->org_col_wu_y * wu_y + g->col_i * i + g->col_j * j;
+            for (int k = 0; k < x->K; k++) {
+                const int64_t r = idx_o + x->dr[k] + pad, c = idx_i + x->dc[k] + pad;
+                if (r < 0 || r >= ah || c < 0 || c >= aw) return ORA_ERR_BOUNDS;
+                if (x->variant == 1) {
+                    const int64_t rr = idx_o + x->dr[k] - org_row, cc = idx_i + x->dc[k] - org_col;
+                    if (rr < 0 || rr >= g->r_rows || cc < 0 || cc >= g->r_cols_pad) return ORA_ERR_BOUNDS;
+                }
+                a = a + hash_at(r * aw + c, 0);
+            }
+            for (int k = 0; k < p->num_comp_ilb; k++) {
+                float c1, c2;
+                mad_constants(k, &c1, &c2);
+                a = a * c1 + c2;
+            }
+            for (int k = 0; k < p->num_coal_ilb; k++)
+                a = a + hash_at(((i * p->m + j + k) % in2_h) * in2_w + glin % in2_w, 1);
+            for (int k = 0; k < p->num_uncoal_ilb; k++)
+                a = a + hash_at((glin % in2_h) * in2_w + (i * p->m + j + k) % in2_w, 1);
+        }
+    }
+    for (int k = 0; k < p->num_comp_ep; k++) {
+        float c1, c2;
+        mad_constants(p->num_comp_ilb + k, &c1, &c2);
+        a = a * c1 + c2;
+    }
+    for (int k = 0; k < p->num_coal_ep; k++)
+        a = a + hash_at((((int64_t)p->n * p->m + k) % in2_h) * in2_w + glin % in2_w, 1);
+    for (int k = 0; k < p->num_uncoal_ep; k++)
+        a = a + hash_at((glin % in2_h) * in2_w + ((int64_t)p->n * p->m + k) % in2_w, 1);
+    *val = a;
+    return ORA_OK;
+}
+
+static void *eval_worker(void *arg) {
+    eval_ctx *x = (eval_ctx *)arg;
+    for (int64_t k = x->tid; k < x->count; k += x->nthreads) {
+        int rc = eval_one(x, x->idx[k], &x->vals[k]);
+        if (rc != ORA_OK) {
+            x->err = rc;
+            return NULL;
+        }
+    }
+    return NULL;
+}
+
+int ora_eval_units(const ora_instance *p, const ora_device *dev, int variant, const int64_t *idx, int64_t count,
+                   float *vals, int nthreads) {
+    if (ora_validate(p) != 0) return ORA_ERR_INVALID;
+    ora_geometry g;
+    int rc = ora_geometry_of(p, dev, &g);
+    if (rc != ORA_OK) return rc;
+    for (int64_t k = 0; k < count; k++)
+        if (idx[k] < 0 || idx[k] >= (int64_t)p->out_h * p->out_w) return ORA_ERR_ARG;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    if (nthreads > count) nthreads = count > 0 ? (int)count : 1;
+    eval_ctx *ctx = (eval_ctx *)calloc((size_t)nthreads, sizeof(eval_ctx));
+    pthread_t tids[256];
+    for (int t = 0; t < nthreads; t++) {
+        ctx[t].p = p;
+        ctx[t].g = g;
+        ctx[t].variant = variant;
+        ctx[t].idx = idx;
+        ctx[t].count = count;
+        ctx[t].vals = vals;
+        ctx[t].K = ora_stencil_offsets(p->stencil_shape, p->stencil_radius, ctx[t].dr, ctx[t].dc, 1024);
+        ctx[t].tid = t;
+        ctx[t].nthreads = nthreads;
+        pthread_create(&tids[t], NULL, eval_worker, &ctx[t]);
+    }
+    rc = ORA_OK;
+    for (int t = 0; t < nthreads; t++) {
+        pthread_join(tids[t], NULL);
+        if (ctx[t].err) rc = ctx[t].err;
+    }
+    free(ctx);
+    return rc;
 }

@@ -72,9 +72,16 @@ int ora_execute(const ora_instance *inst, const ora_device *dev, int variant,
                 const float *in, int64_t in_rows, int64_t in_cols,
                 const float *in2, float *out, int nthreads,
                 int64_t wg_begin, int64_t wg_end);
+int ora_execute_prefix(const ora_instance *p, const ora_device *dev, int variant, const float *in, int64_t in_rows,
+                       int64_t in_cols, const float *in2, float *out, int nthreads, int64_t wg_begin, int64_t wg_end,
+                       int64_t units_per_wg);
 uint64_t ora_out_hash(const float *out, int64_t count);
 int64_t ora_execute_sample(const ora_instance *p, const ora_device *dev, int variant, const float *in,
                            int64_t in_rows, int64_t in_cols, const float *in2, float *out, int64_t max_units);
+/* interp.execute's value at out[idx[k] / out_w][idx[k] % out_w] for each k,
+ * with make_inputs' hash evaluated on the fly (see lmt_oracle.c). */
+int ora_eval_units(const ora_instance *p, const ora_device *dev, int variant, const int64_t *idx, int64_t count,
+                   float *vals, int nthreads);
 int ora_forest_mean(const int32_t *feature, const double *threshold,
                     const int32_t *left, const int32_t *right, const double *value,
                     const int64_t *tree_off, int32_t ntrees,

@@ -26,6 +26,9 @@ LMT_ERR_TOO_LARGE = 5
 
 MEASURE_SKIP_OPT = 0x1
 MEASURE_ALLOW_LARGE_LMEM = 0x4
+MEASURE_CONCURRENT = 0x8
+MEASURE_REGBLOCK = 0x10
+MEASURE_WARM_L2 = 0x20
 
 INSTANCE_FIELDS = (
     "in_h", "in_w", "out_h", "out_w", "pattern", "n", "m", "stencil_shape",
@@ -74,6 +77,15 @@ class CMeasurement(ctypes.Structure):
         ("alg_flops", ctypes.c_double), ("t_fill_ms", ctypes.c_double),
         ("status", ctypes.c_int32), ("kernel_id", ctypes.c_int32),
         ("launches", ctypes.c_int32), ("nstages", ctypes.c_int32),
+        ("lane_sms", ctypes.c_int32), ("order", ctypes.c_int32),
+        ("in_copies", ctypes.c_int32), ("ctas", ctypes.c_int32),
+    ]
+
+
+class CMeasureOpts(ctypes.Structure):
+    _fields_ = [
+        ("flags", ctypes.c_int32), ("samples", ctypes.c_int32),
+        ("sample_idx", ctypes.c_void_p), ("h_sample_vals", ctypes.c_void_p),
     ]
 
 
@@ -84,6 +96,7 @@ EXPORTS = (
     "lmt_rf_create", "lmt_rf_mean", "lmt_rf_mean_host", "lmt_rf_destroy", "lmt_sync",
     "lmt_get_stream", "lmt_prepare", "lmt_jit_stats", "lmt_features", "lmt_real_validate",
     "lmt_real_execute", "lmt_real_measure", "lmt_rf_train_tree", "lmt_kernel_source",
+    "lmt_measure_batch_ex", "lmt_partitions",
 )
 
 _lib = None
@@ -106,6 +119,11 @@ def _declare(L):
         P(CInstance), c_i64, P(CDevice), c_i32, P(vp), P(c_i64), P(c_i64), P(vp), P(vp), P(vp),
         P(CMeasurement),
     ]
+    L.lmt_measure_batch_ex.argtypes = [
+        P(CInstance), c_i64, P(CDevice), P(CMeasureOpts), P(vp), P(c_i64), P(c_i64), P(vp), P(vp), P(vp),
+        P(CMeasurement),
+    ]
+    L.lmt_partitions.argtypes = [P(c_i32), c_i32, P(c_i32)]
     L.lmt_digest.argtypes = [vp, c_i64, P(ctypes.c_uint64), vp]
     L.lmt_rf_create.argtypes = [vp, vp, vp, vp, vp, vp, c_i32, c_i32, P(vp)]
     L.lmt_rf_mean.argtypes = [vp, vp, c_i64, vp, vp, vp]
@@ -121,7 +139,7 @@ def _declare(L):
     L.lmt_real_measure.argtypes = [P(CRealInstance), c_i64, c_i32, P(CMeasurement)]
     L.lmt_rf_train_tree.argtypes = [vp, vp, c_i64, c_i32, vp, c_i64, vp, c_i64, c_i32, c_i32, c_i32, vp, vp, vp,
                                     vp, vp, c_i64, P(c_i64), P(c_i64)]
-    L.lmt_kernel_source.argtypes = [P(CInstance), P(CDevice), ctypes.c_int, ctypes.c_char_p, c_i64, P(c_i64)]
+    L.lmt_kernel_source.argtypes = [P(CInstance), P(CDevice), ctypes.c_int, c_i32, ctypes.c_char_p, c_i64, P(c_i64)]
     L.lmt_features.argtypes = [P(CInstance), c_i64, P(CDevice), c_i64, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         fn = getattr(L, name)
@@ -177,6 +195,15 @@ def library_stream() -> int:
     s = ctypes.c_void_p()
     check(lib().lmt_get_stream(ctypes.byref(s)), what="get_stream")
     return int(s.value or 0)
+
+
+def partitions() -> list[int]:
+    """SM counts of the partitions MEASURE_CONCURRENT runs in on the current
+    device (empty: no green contexts, every instance runs on the whole device)."""
+    sizes = (ctypes.c_int32 * 64)()
+    n = ctypes.c_int32()
+    check(lib().lmt_partitions(sizes, 64, ctypes.byref(n)), what="partitions")
+    return [int(sizes[k]) for k in range(n.value)]
 
 
 def jit_stats() -> tuple[int, float]:

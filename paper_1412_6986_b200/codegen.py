@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
-from ._lib import check, lib
+from ._lib import MEASURE_REGBLOCK, check, lib
 from .device import DEFAULT_DEVICE
 from .errors import OptimizationInfeasible
 from .geometry import Variant, c_device, footprint
@@ -30,14 +30,15 @@ class KernelSource:
     compile_defines: tuple
 
 
-def _source(instance, variant: Variant, dev) -> KernelSource:
+def _source(instance, variant: Variant, dev, regblock: bool) -> KernelSource:
     L = lib()
     n = ctypes.c_int64()
     vid = 0 if variant is Variant.BASELINE else 1
-    check(L.lmt_kernel_source(ctypes.byref(to_c(instance)), ctypes.byref(c_device(dev)), vid, None, 0,
+    flags = MEASURE_REGBLOCK if regblock else 0
+    check(L.lmt_kernel_source(ctypes.byref(to_c(instance)), ctypes.byref(c_device(dev)), vid, flags, None, 0,
                               ctypes.byref(n)), what="kernel_source")
     buf = ctypes.create_string_buffer(n.value + 1)
-    check(L.lmt_kernel_source(ctypes.byref(to_c(instance)), ctypes.byref(c_device(dev)), vid, buf, len(buf),
+    check(L.lmt_kernel_source(ctypes.byref(to_c(instance)), ctypes.byref(c_device(dev)), vid, flags, buf, len(buf),
                               ctypes.byref(n)), what="kernel_source")
     text = buf.value.decode()
     defines = []
@@ -49,19 +50,21 @@ def _source(instance, variant: Variant, dev) -> KernelSource:
     return KernelSource(variant, "lmt_kernel", text, tuple(defines))
 
 
-def emit_baseline(instance, dev=DEFAULT_DEVICE) -> KernelSource:
-    """codegen.py:336-340; raises InvalidInstance on constraint violations."""
-    return _source(instance, Variant.BASELINE, dev)
+def emit_baseline(instance, dev=DEFAULT_DEVICE, *, regblock: bool = False) -> KernelSource:
+    """codegen.py:336-340; raises InvalidInstance on constraint violations.
+    ``regblock``: the register-blocked kernel (LMT_MEASURE_REGBLOCK) instead
+    of the literal one."""
+    return _source(instance, Variant.BASELINE, dev, regblock)
 
 
-def emit_optimized(instance, fp=None, dev=DEFAULT_DEVICE) -> KernelSource:
+def emit_optimized(instance, fp=None, dev=DEFAULT_DEVICE, *, regblock: bool = False) -> KernelSource:
     """codegen.py:343-354; raises OptimizationInfeasible when the staging
     region exceeds the device's local-memory capacity."""
     if fp is None:
         fp = footprint(instance, dev)
     if fp.bytes > dev.lmem_capacity_bytes:
         raise OptimizationInfeasible(fp.bytes, dev.lmem_capacity_bytes)
-    return _source(instance, Variant.OPTIMIZED, dev)
+    return _source(instance, Variant.OPTIMIZED, dev, regblock)
 
 
 def defines_manifest(source: KernelSource) -> str:

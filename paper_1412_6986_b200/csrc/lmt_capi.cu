@@ -1,6 +1,7 @@
 // lmt_capi.cu -- host side of liblmt_b200.so: the C ABI declared in
 // include/lmt_b200.h. Validation, geometry, device-memory cache, TMA
-// descriptor encoding, kernel dispatch and CUDA-event timing.
+// descriptor encoding, kernel dispatch, the measurement engine (CUDA-event
+// timing on the whole device or in SM partitions) and the ABI wrappers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -11,13 +12,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/lmt_b200.h"
 #include "lmt_kernels.cuh"
-#include "lmt_synth_ilp.cuh"
 #include "lmt_jit_host.cuh"
 #include "lmt_features.cuh"
 #include "lmt_real.cuh"
@@ -188,128 +190,108 @@ int compute_geometry(const lmt_instance &p, const lmt_device &d, lmt_geometry *g
     return LMT_OK;
 }
 
-// ------------------------------------------------------ kernel dispatch
-
-using BaseFn = void (*)(const SynthArgs);
-using OptFn = void (*)(const CUtensorMap, const SynthArgs);
-
-struct KernelSet {
-    BaseFn base;
-    OptFn opt;
-    OptFn opt_wide;
-};
-
-// stencil ids: 0 point, 1 star1 (== diamond1), 2 star2, 3 diamond2, 4 rect1, 5 rect2, 6 generic
-const KernelSet kKernels[7] = {
-    {k_synth_base<0, 0>, k_synth_opt<0, 0, false>, k_synth_opt<0, 0, true>},
-    {k_synth_base<2, 1>, k_synth_opt<2, 1, false>, k_synth_opt<2, 1, true>},
-    {k_synth_base<2, 2>, k_synth_opt<2, 2, false>, k_synth_opt<2, 2, true>},
-    {k_synth_base<1, 2>, k_synth_opt<1, 2, false>, k_synth_opt<1, 2, true>},
-    {k_synth_base<0, 1>, k_synth_opt<0, 1, false>, k_synth_opt<0, 1, true>},
-    {k_synth_base<0, 2>, k_synth_opt<0, 2, false>, k_synth_opt<0, 2, true>},
-    {k_synth_base<-1, -1>, k_synth_opt<-1, -1, false>, k_synth_opt<-1, -1, true>},
-};
-
-// Grouped (ILP) kernels for the compile-time stencils, U = 1, 2, 4.
-struct KernelSetG {
-    BaseFn base[3];
-    OptFn opt[3];
-};
-#define LMT_G(SH, RR)                                                                                  \
-    {{k_synth_base_g<SH, RR, 1>, k_synth_base_g<SH, RR, 2>, k_synth_base_g<SH, RR, 4>},                \
-     {k_synth_opt_g<SH, RR, 1>, k_synth_opt_g<SH, RR, 2>, k_synth_opt_g<SH, RR, 4>}}
-const KernelSetG kKernelsG[6] = {LMT_G(0, 0), LMT_G(2, 1), LMT_G(2, 2), LMT_G(1, 2), LMT_G(0, 1), LMT_G(0, 2)};
-#undef LMT_G
-
-int u_index(int U) { return U == 4 ? 2 : (U == 2 ? 1 : 0); }
-
-int stencil_id(int shape, int r) {
-    if (r == 0) return 0;
-    if (r == 1) return shape == 0 ? 4 : 1;
-    if (r == 2) return shape == 0 ? 5 : (shape == 1 ? 3 : 2);
-    return 6;
-}
-
 // ------------------------------------------------------- device context
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+// Driver entry points of the green-context (SM partition) API, resolved at
+// run time like the TMA encoder (no libcuda at link time).
+struct GreenApi {
+    PFN_cuDeviceGet_v2000 device_get = nullptr;
+    PFN_cuDeviceGetDevResource_v12040 get_resource = nullptr;
+    PFN_cuDevSmResourceSplitByCount_v12040 split = nullptr;
+    PFN_cuDevResourceGenerateDesc_v12040 gen_desc = nullptr;
+    PFN_cuGreenCtxCreate_v12040 create = nullptr;
+    PFN_cuGreenCtxStreamCreate_v12050 stream_create = nullptr;
+    PFN_cuCtxFromGreenCtx_v12040 to_ctx = nullptr;
+    bool tried = false, ok = false;
+} g_green;
+
+PFN_cuCtxGetCurrent_v4000 g_ctx_current = nullptr;
+
+bool green_init() {
+    if (g_green.tried) return g_green.ok;
+    g_green.tried = true;
+    struct {
+        const char *name;
+        void **slot;
+    } fns[] = {{"cuDeviceGet", (void **)&g_green.device_get},
+               {"cuDeviceGetDevResource", (void **)&g_green.get_resource},
+               {"cuDevSmResourceSplitByCount", (void **)&g_green.split},
+               {"cuDevResourceGenerateDesc", (void **)&g_green.gen_desc},
+               {"cuGreenCtxCreate", (void **)&g_green.create},
+               {"cuGreenCtxStreamCreate", (void **)&g_green.stream_create},
+               {"cuCtxFromGreenCtx", (void **)&g_green.to_ctx}};
+    for (auto &f : fns) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(f.name, f.slot, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !*f.slot)
+            return false;
+    }
+    g_green.ok = true;
+    return true;
+}
+
+// Where instances run: the whole device (isolated: one instance at a time,
+// L2 flushed before each variant), or one SM partition (a green context).
+// A lane owns its input/output buffers; its stream orders its instances.
+struct Lane {
+    int sms = 0;  // SMs of the partition; 0 = the whole device
+    cudaStream_t s = nullptr;
+    CUcontext ctx = nullptr;  // the (green) context its stream belongs to
+    // host mode: the copied `in` (+ the baseline's shifted copies); device
+    // mode: the baseline's shifted copies of the shared `in` only
+    float *in[2] = {nullptr, nullptr};
+    size_t in_cap[2] = {0, 0};
+    float *ob[2] = {nullptr, nullptr}, *oo[2] = {nullptr, nullptr};
+    size_t out_cap[2] = {0, 0};
+    float *in2[2] = {nullptr, nullptr};  // host mode: this lane's in2 in the kernels' layout
+    size_t in2_cap[2] = {0, 0};
+    // host mode on the whole device: copies on their own streams, two buffer
+    // sets, so the copies of instances i +- 1 overlap the kernels of i
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t copied[2] = {}, consumed[2] = {}, drained[2] = {};
+    std::vector<int64_t> inflight;  // instances enqueued, in order
+};
 
 struct DevCtx {
     int device = -1;
     int sms = 0;
     size_t smem_optin = 0;
-    cudaStream_t stream = nullptr;
-    float *in = nullptr;
-    size_t in_cap = 0;          // floats
-    int64_t in_rows = -1, in_cols = -1, in_pitch = -1;
-    int in_copies = 0;
-    float *in2 = nullptr;
-    size_t in2_cap = 0;
-    int64_t in2_h = -1, in2_w = -1;
-    float *outb = nullptr, *outo = nullptr;
-    size_t outb_cap = 0, outo_cap = 0;
+    cudaStream_t stream = nullptr;  // the library stream: the whole-device lane
+    Lane full;
+    std::vector<Lane> parts;        // SM partitions, largest first
+    bool parts_tried = false;
+    // device-generated inputs, shared read-only by every lane: `in` per
+    // logical width (its content is hash(r * alloc_w + c) whatever the
+    // instance), in2 per shape in the kernels' wrapped-halo layout
+    struct SharedIn {
+        float *p = nullptr;
+        int64_t rows = 0, pitch = 0;
+        uint64_t used = 0;
+    };
+    std::map<int64_t, SharedIn> ins;
+    size_t ins_bytes = 0;
+    uint64_t batch_no = 0;
+    std::map<std::pair<int64_t, int64_t>, float *> in2s;
+    cudaEvent_t inputs_ready = nullptr;  // shared inputs and per-batch scratch are ready
+    float4 *scrub = nullptr;        // L2 flush buffer
+    int64_t scrub_n4 = 0;
+    float scrub_tag = 0.0f;
     unsigned long long *dres = nullptr;
-    size_t dres_cap = 0;        // instances
+    size_t dres_cap = 0;
+    int64_t *didx = nullptr;
+    size_t didx_cap = 0;
+    float *dsamp = nullptr;
+    size_t dsamp_cap = 0;
     std::vector<cudaEvent_t> events;
-    bool attrs_set = false;
-    // host-buffer measurement: two slots of device inputs/outputs so the
-    // copies of instance i +- 1 (own streams) overlap the kernels of instance i
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t copied[2] = {}, consumed[2] = {}, drained[2] = {};
-    float *hin[2] = {}, *hin2[2] = {}, *hob[2] = {}, *hoo[2] = {};
-    size_t hin_cap[2] = {}, hin2_cap[2] = {}, hob_cap[2] = {}, hoo_cap[2] = {};
 };
 
 std::mutex g_mu;
 DevCtx g_ctx[64];
 
-int get_ctx(DevCtx **out) {
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64) return fail(LMT_ERR_ARG, "device %d out of range", dev);
-    DevCtx &c = g_ctx[dev];
-    if (c.device < 0) {
-        CUDA_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
-        int optin = 0;
-        CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        c.smem_optin = (size_t)optin;
-        CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-        CUDA_TRY(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
-        CUDA_TRY(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
-        for (int b = 0; b < 2; b++) {
-            CUDA_TRY(cudaEventCreateWithFlags(&c.copied[b], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&c.consumed[b], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&c.drained[b], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventRecord(c.consumed[b], c.stream));  // complete: nothing in flight yet
-            CUDA_TRY(cudaEventRecord(c.drained[b], c.stream));
-        }
-        c.device = dev;
-    }
-    if (!g_encode) {
-        void *fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) return fail(LMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    if (!c.attrs_set) {
-        for (auto &k : kKernels) {
-            CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
-            CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt_wide),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
-        }
-        for (auto &k : kKernelsG)
-            for (int u = 0; u < 3; u++)
-                CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k.opt[u]),
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem_optin - 1024));
-        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_rf_mean),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-        c.attrs_set = true;
-    }
-    *out = &c;
-    return LMT_OK;
-}
+constexpr int kEvPerInst = 8;  // base start/end, opt start/end, done, fill start/end, spare
+constexpr int64_t kScrubBytes = 192ll << 20;  // > 126 MB L2
 
 template <class T>
 int ensure(T **p, size_t *cap, size_t need) {
@@ -322,21 +304,142 @@ int ensure(T **p, size_t *cap, size_t need) {
     return LMT_OK;
 }
 
+int lane_streams(Lane &L) {
+    if (L.h2d) return LMT_OK;
+    CUDA_TRY(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; b++) {
+        CUDA_TRY(cudaEventCreateWithFlags(&L.copied[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&L.consumed[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&L.drained[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(L.consumed[b], L.s));  // complete: nothing in flight yet
+        CUDA_TRY(cudaEventRecord(L.drained[b], L.s));
+    }
+    return LMT_OK;
+}
+
+int get_ctx(DevCtx **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(LMT_ERR_ARG, "device %d out of range", dev);
+    DevCtx &c = g_ctx[dev];
+    if (c.device < 0) {
+        CUDA_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+        int optin = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        c.smem_optin = (size_t)optin;
+        CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.full.s = c.stream;
+        CUDA_TRY(cudaFree(0));  // the primary context exists and is current
+        if (!g_ctx_current) {
+            cudaDriverEntryPointQueryResult q;
+            CUDA_TRY(cudaGetDriverEntryPoint("cuCtxGetCurrent", (void **)&g_ctx_current, cudaEnableDefault, &q));
+            if (!g_ctx_current || q != cudaDriverEntryPointSuccess) return fail(LMT_ERR_CUDA, "cuCtxGetCurrent unavailable");
+        }
+        if (g_ctx_current(&c.full.ctx) != CUDA_SUCCESS) return fail(LMT_ERR_CUDA, "no current CUDA context");
+        CUDA_TRY(cudaEventCreateWithFlags(&c.inputs_ready, cudaEventDisableTiming));
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_rf_mean),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_opt),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_rows_opt),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_cols_opt),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        c.device = dev;
+    }
+    if (!g_encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(LMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    *out = &c;
+    return LMT_OK;
+}
+
+// The SM partitions of the concurrent measurement: one split of the device
+// into 2-SM groups (the finest the driver offers), regrouped into
+// partitions of 74, 36, 16, 8, 8, 4 and 2 SMs. The sizes come from a
+// scheduling simulation over the round-1 40k-instance sweep:
+// any layout of this kind packs the sweep within a few percent of the
+// others; what bounds the gain is the launches too wide for a partition.
+const int kLayout[] = {74, 36, 16, 8, 8, 4, 2};
+
+// Module loading is lazy and per context: launch every ahead-of-time kernel
+// a lane uses once, so none of them loads inside a timed window later.
+int warm_lane(Lane &L) {
+    float *buf = nullptr;
+    CUDA_TRY(cudaMalloc(&buf, 4096 * sizeof(float)));
+    int64_t *idx = reinterpret_cast<int64_t *>(buf + 2048);
+    CUDA_TRY(cudaMemsetAsync(buf, 0, 4096 * sizeof(float), L.s));
+    k_fill<<<1, 32, 0, L.s>>>(buf, 1, 4, 4, 0);
+    k_in2_halo<<<1, 32, 0, L.s>>>(buf, 1, 1, 4);
+    k_in2_shift<<<1, 32, 0, L.s>>>(buf, 1, 1, 4, 0);
+    k_in_shift<<<1, 32, 0, L.s>>>(buf, 0, 4);
+    k_in_copy4<<<1, 32, 0, L.s>>>(buf, buf + 512, 0, 4);
+    k_digest<<<1, 32, 0, L.s>>>(buf, buf, 0, reinterpret_cast<unsigned long long *>(buf + 1024));
+    k_gather<<<1, 32, 0, L.s>>>(buf, buf, idx, 0, buf + 1536);
+    k_scrub<<<1, 32, 0, L.s>>>(reinterpret_cast<float4 *>(buf), 0, 0.0f);
+    k_lead<<<1, 32, 0, L.s>>>(0ll);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(L.s));
+    CUDA_TRY(cudaFree(buf));
+    return LMT_OK;
+}
+
+int ensure_parts(DevCtx *c) {
+    if (c->parts_tried) return LMT_OK;
+    c->parts_tried = true;
+    if (!green_init()) return LMT_OK;
+    CUdevice dev;
+    if (g_green.device_get(&dev, c->device) != CUDA_SUCCESS) return LMT_OK;
+    CUdevResource all;
+    if (g_green.get_resource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return LMT_OK;
+    unsigned ng = 0;
+    const unsigned fl = CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
+    if (g_green.split(nullptr, &ng, &all, nullptr, fl, 2) != CUDA_SUCCESS || ng == 0) return LMT_OK;
+    std::vector<CUdevResource> g(ng);
+    CUdevResource rem;
+    if (g_green.split(g.data(), &ng, &all, &rem, fl, 2) != CUDA_SUCCESS) return LMT_OK;
+    const unsigned per = g[0].sm.smCount;
+    unsigned next = 0;
+    for (int size : kLayout) {
+        const unsigned k = (unsigned)size / std::max(1u, per);
+        if (k == 0 || next + k > ng) break;
+        CUdevResourceDesc desc;
+        if (g_green.gen_desc(&desc, &g[next], k) != CUDA_SUCCESS) break;
+        CUgreenCtx gc;
+        if (g_green.create(&gc, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) break;
+        CUstream st;
+        if (g_green.stream_create(&st, gc, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) break;
+        Lane L;
+        L.sms = (int)(k * per);
+        L.s = (cudaStream_t)st;
+        if (g_green.to_ctx(&L.ctx, gc) != CUDA_SUCCESS) break;
+        int rc = warm_lane(L);
+        if (rc) return rc;
+        c->parts.push_back(L);
+        next += k;
+    }
+    return LMT_OK;
+}
+
 // ------------------------------------------------------ launch planning
 
 struct Plan {
     lmt_geometry g;
     SynthArgs A;
-    int sid;
-    int u_base, u_opt;  // work units per thread in lockstep (ILP); 0 = legacy U=1 kernels
     bool feasible;      // footprint <= lmem cap (codegen.py:351)
     bool wide;
-    bool jit;           // NVRTC-specialised kernels (lmt_jit.cuh) instead of the AOT set
-    JitKey kb, ko;      // their keys (baseline, optimized)
+    JitKey kb, ko;      // specialised kernels (baseline, optimized)
     int in_copies;      // shifted copies of `in` the baseline reads (1 or kInCopies)
     size_t dyn_smem;
     dim3 grid, block;
+    int64_t ctas;
     double alg_bytes, alg_flops;
+    double est_s;       // launch floor of one variant (scheduling only)
 };
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
@@ -395,6 +498,7 @@ double in_union(const lmt_instance &p) {
 }
 
 constexpr int kMaxStagesJ = 16;
+constexpr int kPfDist = 8;  // L1 prefetch distance of the in2 context lines, steps
 JitCache g_jit;
 
 // kernel_id of a specialised pair: 1 B D O E with B/O = log2 U + 1 of the
@@ -405,43 +509,18 @@ int jit_kid(const JitKey &b, const JitKey &o) {
     return 10000 + lg(b.U) * 1000 + b.D * 100 + lg(o.U) * 10 + o.D;
 }
 
-int jit_pf() {
-    const char *e = getenv("LMT_PF");
-    const int v = e ? atoi(e) : 8;
-    return std::max(0, std::min(v, kPfMax - 1));
-}
-
-// Largest work-units-per-thread candidate: 16 for the baseline (measured on
-// B200: 10-22 % faster than 8 on launches with one warp per SM
-// sub-partition), 8 for the optimized variant, whose U staged regions per
-// group cost shared memory and hence residency (U = 16 measured up to 2x
-// slower there). LMT_UMAX overrides both.
-int jit_umax(bool opt) {
-    if (const char *e = getenv("LMT_UMAX")) return atoi(e) >= 16 ? 16 : 8;
-    return opt ? 8 : 16;
-}
-
-bool jit_vec() {
-    const char *e = getenv("LMT_VEC");
-    return !(e && e[0] == '0');
-}
-
-bool jit_enabled() {
-    const char *e = getenv("LMT_JIT");
-    return !(e && e[0] == '0');
-}
-
 // Work units per thread U, prefetch depth D (and, for the optimized
 // variant, staging slots S) for the specialised kernels.
 //
 // A thread's work units are independent fp32 chains, so U of them in
 // lockstep give U-way ILP, and the in2 context loads of a step are shared by
-// its U work units (U times fewer context loads and L1 wavefronts per chain
-// operation); D prefetched steps hide load latency. Measured on B200
-// (tools/gpu_ud.sh): the largest U and D the register file holds win on
-// every representative launch shape, from one-thread workgroups to 1024-
-// thread ones, so the baseline asks for U = 8, D = 3 and JitCache::resolve
-// steps D, then U, down until ptxas does not spill.
+// its U work units; D prefetched steps hide load latency. Each work unit
+// still issues its own stencil loads (the emitted kernel's semantics)
+// unless `regblock` lets units with identical home coordinates share them.
+// Measured on B200 (round 1, tools/gpu_ud.sh): the largest U and D the
+// register file holds win on every representative launch shape, so the
+// baseline asks for U = 16, D = 3 and JitCache::resolve steps D, then U,
+// down until ptxas does not spill.
 //
 // The optimized variant also needs S >= U staged regions per CTA (S >= 2U to
 // overlap the next group's TMA with the current group), and shared memory
@@ -457,43 +536,39 @@ int64_t jit_regs_guess(int K, int64_t slot, int U, int D) {
 // it0 % U == 0) read identical `in` values: their home coordinates do not
 // depend on wu_x (a0 = a4 = 0) and either not on wu_y either (xy_reuse) or
 // the group lies in one row of work units (nwx % U == 0, or one row).
-bool jit_share(const SynthArgs &A, int U) {
-    if (U <= 1 || A.a[0] != 0 || A.a[4] != 0) return false;
-    if (const char *e = getenv("LMT_SHARE"); e && e[0] == '0') return false;
+// Only used by the register-blocked variants (LMT_MEASURE_REGBLOCK).
+bool jit_share(const SynthArgs &A, int U, bool regblock) {
+    if (!regblock || U <= 1 || A.a[0] != 0 || A.a[4] != 0) return false;
     return (A.a[1] == 0 && A.a[5] == 0) || A.nwy == 1 || A.nwx % U == 0;
 }
 
 void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, int64_t ctas, int64_t warps,
-                int64_t nit, int64_t sms, bool opt, int64_t stage_bytes, int64_t smem_cap, int *U_out, int *D_out,
-                int *S_out) {
-    // stencil value sets a step holds for U work units
-    auto sets = [&](int U) -> int64_t { return jit_share(A, U) ? 1 : U; };
+                int64_t nit, int64_t sms, bool opt, int64_t stage_bytes, int64_t smem_cap, bool regblock, int *U_out,
+                int *D_out, int *S_out) {
+    auto sets = [&](int U) -> int64_t { return jit_share(A, U, regblock) ? 1 : U; };
     int bu = 1, bd = 3, bs = 1;
-    for (int U : {jit_umax(false), 8, 4, 2, 1})
+    for (int U : {16, 8, 4, 2, 1})
         if (U <= nit) { bu = U; break; }
     if (!opt) {
         // start where the register estimate fits (ptxas has the last word in
         // JitCache::resolve; a good start saves the compiles of the step-down)
         const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
         const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
-        // a lower bound (values in flight + a little): prunes only configs
-        // that cannot fit; the spill check decides the rest
         auto est = [&](int U, int D) { return D * (sets(U) * K + ctx) + U + 16; };
         while (bu > 1 || bd > 1) {
             if (est(bu, bd) <= regcap) break;
             if (bd > 1) bd--;
             else { bu >>= 1; bd = 3; }
         }
-    }
-    if (opt) {
+    } else {
         bd = 2;  // shared-memory loads: one step of lookahead covers them
         double best = -1.0;
-        for (int U : {jit_umax(true), 8, 4, 2, 1}) {
+        for (int U : {8, 4, 2, 1}) {
             if (U > nit) continue;
             const int64_t slot = sets(U) * K + p.num_coal_ilb + p.num_uncoal_ilb;
             const int64_t regs = std::min<int64_t>(jit_regs_guess(K, slot, U, 2), 65536 / maxt);
             const int64_t rregs = (regs + 7) / 8 * 8;
-            const bool sh = jit_share(A, U);
+            const bool sh = jit_share(A, U, regblock);
             for (int Sx : {2 * U, U + 1, U}) {
                 if (Sx == U + 1 && (!sh || U == 1)) continue;
                 const int64_t S = std::min<int64_t>({(int64_t)Sx, kMaxStagesJ, std::max<int64_t>(nit, 1)});
@@ -518,32 +593,34 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
     {
         const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
         auto step_instr = [&](int U) {
-            return 1.1 * U * (K + p.num_comp_ilb + ctx) + (jit_share(A, U) ? 0.0 : 0.8 * U * K) + ctx;
+            return 1.1 * U * (K + p.num_comp_ilb + ctx) + (jit_share(A, U, regblock) ? 0.0 : 0.8 * U * K) + ctx;
         };
         while (bd > 1 && bd * step_instr(bu) > kLoopInstrBudget) bd--;
-    }
-    if (const char *fu = getenv("LMT_FORCE_U")) {
-        const int f = atoi(fu);
-        if (f == 1 || f == 2 || f == 4 || f == 8 || f == 16) bu = (int)std::min<int64_t>(f, std::max<int64_t>(1, nit));
-    }
-    if (const char *fd = getenv("LMT_FORCE_D")) {
-        const int f = atoi(fd);
-        if (f >= 1 && f <= 4) bd = f;
     }
     if (opt) {
         bs = std::max(bs, bu);
         while (bs > bu && (int64_t)bs * stage_bytes > smem_cap) bs--;
-        if (const char *fs = getenv("LMT_FORCE_STAGES")) {
-            const int f = atoi(fs);
-            if (f >= bu && f <= kMaxStagesJ && (int64_t)f * stage_bytes <= smem_cap) bs = f;
-        }
     }
     *U_out = bu;
     *D_out = bd;
     *S_out = bs;
 }
 
-int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan *pl, DevCtx *ctx) {
+// Launch floor of one variant (sweep.floor_seconds): the per-thread chain,
+// the per-SM issue of the CTAs' warps, and the algorithmic bytes at HBM
+// speed -- used to order and place instances, never as a result.
+double launch_floor_s(const lmt_instance &p, int K, int64_t ctas, int64_t warps, double bytes, int sms) {
+    const double chain = (double)p.n * p.m * (K + p.num_comp_ilb + p.num_coal_ilb + p.num_uncoal_ilb) +
+                         p.num_comp_ep + p.num_coal_ep + p.num_uncoal_ep;
+    const double wus = (double)p.out_h * p.out_w / std::max<double>(1.0, (double)p.grid_x * p.grid_y);
+    const double clk = 1.965e9;
+    const double chain_s = wus * chain / clk;
+    const double issue_s = std::ceil((double)ctas / sms) * warps * wus * chain / 4.0 / clk;
+    return std::max({chain_s, issue_s, bytes / 6.5e12}) + 3e-6;
+}
+
+int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int32_t flags, const DevCtx *ctx,
+              Plan *pl) {
     std::vector<std::string> v = violations(p);
     if (!v.empty()) {
         std::string m;
@@ -556,11 +633,8 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     if (g.alloc_h * in_pitch >= (int64_t)1 << 31 || (int64_t)p.in_h * p.in_w >= (int64_t)1 << 31 ||
         (int64_t)p.out_h * p.out_w >= (int64_t)1 << 31)
         return fail(LMT_ERR_TOO_LARGE, "arrays exceed 2^31 elements");
-    std::vector<int> dr, dc;
-    const int K = stencil_offsets(p.stencil_shape, p.stencil_radius, &dr, &dc);
-    pl->sid = stencil_id(p.stencil_shape, p.stencil_radius);
-    if (pl->sid == 6 && K > kMaxGenericOffsets && !jit_enabled())
-        return fail(LMT_ERR_TOO_LARGE, "stencil has %d > %d points", K, kMaxGenericOffsets);
+    const bool regblock = (flags & LMT_MEASURE_REGBLOCK) != 0;
+    const int K = stencil_offsets(p.stencil_shape, p.stencil_radius, nullptr, nullptr);
     SynthArgs &A = pl->A;
     memset(&A, 0, sizeof A);
     A.P = (int32_t)in_pitch;
@@ -572,14 +646,6 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     A.M = p.m;
     A.nwx = p.out_w / p.grid_x;
     A.nwy = p.out_h / p.grid_y;
-    A.comp_q = p.num_comp_ilb / 10;
-    A.comp_rem = p.num_comp_ilb % 10;
-    A.comp_ep = p.num_comp_ep;
-    A.comp_ep_phase = p.num_comp_ilb % 10;
-    A.coal_ilb = p.num_coal_ilb;
-    A.coal_ep = p.num_coal_ep;
-    A.uncoal_ilb = p.num_uncoal_ilb;
-    A.uncoal_ep = p.num_uncoal_ep;
     const int64_t nm = (int64_t)p.n * p.m;
     A.ep_row0 = (int32_t)(nm % p.in_h);
     A.ep_col0 = (int32_t)(nm % p.in_w);
@@ -588,9 +654,6 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     A.pad = g.pad;
     A.off_min_row = g.off_min_row;
     A.off_min_col = g.off_min_col;
-    A.K = K;
-    if (pl->sid == 6 && K <= kMaxGenericOffsets)
-        for (int k = 0; k < K; k++) { A.sdr[k] = (int8_t)dr[k]; A.sdc[k] = (int8_t)dc[k]; }
     pl->block = dim3(p.wg_x, p.wg_y);
     pl->grid = dim3(p.grid_x / p.wg_x, p.grid_y / p.wg_y);
     pl->feasible = g.footprint_bytes <= d.lmem_capacity_bytes;
@@ -620,99 +683,66 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, Plan
     const int64_t stage_floats = ncc * nrc * bh * bw;
     A.stage_floats = (int32_t)stage_floats;
     A.stage_bytes = (uint32_t)(stage_floats * 4);
-    // stages: prefer overlap (>=2) and fill what the target occupancy leaves
     const int64_t nit = (int64_t)A.nwx * A.nwy;
     const int64_t warps = ((int64_t)p.wg_x * p.wg_y + 31) / 32;
     const int64_t ctas = (int64_t)pl->grid.x * pl->grid.y;
+    pl->ctas = ctas;
     const int64_t sms = ctx ? ctx->sms : 148;
-    int64_t want = std::min<int64_t>({32, std::max<int64_t>(1, 64 / warps), std::max<int64_t>(1, (ctas + sms - 1) / sms)});
     const int64_t smem_cap = ctx ? (int64_t)ctx->smem_optin - 1024 : 227 * 1024;
-    const int64_t budget = (228 * 1024) / want - 1024;
-    int64_t S = std::max<int64_t>(1, std::min<int64_t>(kMaxStages, budget / std::max<int64_t>(1, A.stage_bytes)));
-    if (S < 2 && 2 * (int64_t)A.stage_bytes <= smem_cap) S = 2;
-    S = std::max<int64_t>(1, std::min<int64_t>(S, nit));
-    while (S > 1 && S * (int64_t)A.stage_bytes > smem_cap) S--;
-    if (const char *fs = getenv("LMT_FORCE_STAGES")) {  // debugging aid
-        const int64_t f = atoi(fs);
-        if (f >= 1 && f <= kMaxStages && f * (int64_t)A.stage_bytes <= smem_cap) S = std::min<int64_t>(f, std::max<int64_t>(1, nit));
-    }
-    // ILP: few resident warps -> several work units per thread in lockstep
     const int64_t wgs = (int64_t)p.wg_x * p.wg_y;
-    const double per_smsp = (double)(ctas * warps) / (double)(sms * 4);
-    int U = per_smsp < 2.0 ? 4 : (per_smsp < 4.0 ? 2 : 1);
-    while (U > 1 && (wgs > bound_threads(U, K) || U > nit)) U >>= 1;
-    if (const char *fu = getenv("LMT_FORCE_U")) {  // debugging / tuning aid
-        const int f = atoi(fu);
-        if ((f == 1 || f == 2 || f == 4) && wgs <= bound_threads(f, K)) U = f;
-    }
-    const bool grouped = pl->sid < 6 && !pl->wide;
-    pl->u_base = grouped ? U : 0;
-    if (grouped) {
-        // grouped K2 keeps up to 8 regions in flight; a group needs U slots, overlap needs 2U
-        int64_t S8 = std::max<int64_t>(1, std::min<int64_t>(kMaxStagesG, budget / std::max<int64_t>(1, A.stage_bytes)));
-        while (S8 > 1 && S8 * (int64_t)A.stage_bytes > smem_cap) S8--;
-        int Uo = U;
-        while (Uo > 1 && 2 * Uo > S8) Uo >>= 1;
-        S8 = std::max<int64_t>(1, std::min<int64_t>(S8, std::max<int64_t>(nit, 1)));
-        if (S8 < 2 && nit > 1 && 2 * (int64_t)A.stage_bytes <= smem_cap) S8 = 2;
-        if (const char *fs = getenv("LMT_FORCE_STAGES")) {
-            const int64_t f = atoi(fs);
-            if (f >= Uo && f <= kMaxStagesG && f * (int64_t)A.stage_bytes <= smem_cap) S8 = f;
-        }
-        S = S8;
-        pl->u_opt = Uo;
-    } else {
-        pl->u_opt = 0;
-    }
-    // NVRTC-specialised kernels: every stencil, straight-line step bodies
-    pl->jit = jit_enabled();
-    if (pl->jit) {
-        const int64_t maxt = wgs <= 256 ? 256 : (wgs <= 512 ? 512 : 1024);
-        const bool ctxwrap = p.num_coal_ilb > kIn2HaloRows || p.num_coal_ep > kIn2HaloRows ||
-                             p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
-        JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
-                  p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
-                  p.in_h, p.in_w, (int)in2_pitch(p.in_w), jit_pf(), 0, 1, 0};
-        // 128-bit stencil-row loads in the baseline need rows of >= 5 taps (radius >= 2)
-        k0.vec = (p.stencil_radius >= 2 && jit_vec()) ? 1 : 0;
-        int Ub, Db, Uo, Do, Sb, So;
-        // Baseline launches with few work units per thread (U <= 2) and CTAs to
-        // spare get their ILP from resident warps instead: launch bounds that
-        // keep 32 warps per SM resident (8 per scheduler) cap the registers.
-        int64_t maxt_b = maxt, minb = 1;
-        if (nit <= 2 && ctas >= 2 * sms && !getenv("LMT_NO_MINB")) {
-            minb = std::min<int64_t>({(32 + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
-                                      ctas / std::max<int64_t>(1, sms)});
-            if (minb > 1) maxt_b = warps * 32;
-            else minb = 1;
-        }
-        choose_jit(K, p, A, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, &Ub, &Db, &Sb);
-        choose_jit(K, p, A, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, &Uo, &Do, &So);
-        S = So;
-        pl->kb = k0;
-        pl->kb.maxt = (int)maxt_b;
-        pl->kb.minb = (int)minb;
-        pl->kb.U = Ub;
-        pl->kb.D = Db;
-        pl->kb.share = jit_share(A, Ub) ? 1 : 0;  // stays valid when the spill step-down halves U
-        pl->ko = k0;
-        pl->ko.U = Uo;
-        pl->ko.D = Do;
-        pl->ko.opt = 1;
-        pl->ko.share = jit_share(A, Uo) ? 1 : 0;
-        pl->ko.wide = pl->wide ? 1 : 0;
-        pl->u_base = Ub;
-        pl->u_opt = Uo;
-    }
-    pl->in_copies = (pl->jit && pl->kb.vec) ? kInCopies : 1;
-    A.nstages = (int32_t)S;
-    pl->dyn_smem = (size_t)S * A.stage_bytes;
-    if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
+    const int64_t maxt = wgs <= 256 ? 256 : (wgs <= 512 ? 512 : 1024);
+    const bool ctxwrap = p.num_coal_ilb > kIn2HaloRows || p.num_coal_ep > kIn2HaloRows ||
+                         p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
+    JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
+              p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
+              p.in_h, p.in_w, (int)in2_pitch(p.in_w), kPfDist, 0, 1, 0};
 
     pl->alg_bytes = 4.0 * (in_union(p) + in2_union(p) + (double)p.out_h * p.out_w);
     const double per_wu = (double)nm * (K + 2.0 * p.num_comp_ilb + p.num_coal_ilb + p.num_uncoal_ilb) +
                           2.0 * p.num_comp_ep + p.num_coal_ep + p.num_uncoal_ep;
     pl->alg_flops = per_wu * p.out_h * p.out_w;
+    pl->est_s = launch_floor_s(p, K, ctas, warps, pl->alg_bytes, (int)sms);
+
+    // 128-bit stencil-row loads (rows of >= 5 taps, radius >= 2) read three
+    // shifted copies of `in` that the baseline builds inside its own timed
+    // window (k_in_shift); used only where that copy is cheap next to the
+    // launch (<= 2% of its floor, at the bandwidth share of its SMs).
+    if (p.stencil_radius >= 2) {
+        const double shift_bytes = 6.0 * 4.0 * (double)g.alloc_h * (double)in_pitch;  // 3 copies, read + write
+        const double bw_share = 6.0e12 * std::min<double>(1.0, std::max<double>(8.0, (double)ctas) / (double)sms);
+        k0.vec = shift_bytes / bw_share <= 0.02 * pl->est_s ? 1 : 0;
+    }
+    // Baseline launches with few work units per thread (U <= 2) and CTAs to
+    // spare get their ILP from resident warps instead: launch bounds that
+    // keep 32 warps per SM resident (8 per scheduler) cap the registers.
+    int64_t maxt_b = maxt, minb = 1;
+    if (nit <= 2 && ctas >= 2 * sms) {
+        minb = std::min<int64_t>({(32 + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
+                                  ctas / std::max<int64_t>(1, sms)});
+        if (minb > 1) maxt_b = warps * 32;
+        else minb = 1;
+    }
+    int Ub, Db, Uo, Do, Sb, So;
+    choose_jit(K, p, A, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, regblock, &Ub, &Db, &Sb);
+    choose_jit(K, p, A, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, regblock, &Uo, &Do,
+               &So);
+    pl->kb = k0;
+    pl->kb.maxt = (int)maxt_b;
+    pl->kb.minb = (int)minb;
+    pl->kb.U = Ub;
+    pl->kb.D = Db;
+    pl->kb.share = jit_share(A, Ub, regblock) ? 1 : 0;  // stays valid when the spill step-down halves U
+    pl->ko = k0;
+    pl->ko.vec = 0;
+    pl->ko.U = Uo;
+    pl->ko.D = Do;
+    pl->ko.opt = 1;
+    pl->ko.share = jit_share(A, Uo, regblock) ? 1 : 0;
+    pl->ko.wide = pl->wide ? 1 : 0;
+    pl->in_copies = pl->kb.vec ? kInCopies : 1;
+    A.nstages = (int32_t)So;
+    pl->dyn_smem = (size_t)So * A.stage_bytes;
+    if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
     return LMT_OK;
 }
 
@@ -729,58 +759,59 @@ int encode_tmap(CUtensorMap *map, const float *d_in, int64_t rows, int64_t cols,
     return LMT_OK;
 }
 
-// d_in2x: in2 in the wrapped-halo layout (k_in2_halo), pitch in2_pitch(in_w)
-int launch_variant(const Plan &pl0, int variant, const float *d_in, int64_t in_rows, int64_t in_cols, int64_t pitch,
-                   const float *d_in2x, float *d_out, cudaStream_t s) {
-    Plan pl = pl0;
-    pl.A.in = d_in;
-    pl.A.in_copy = pl.in_copies > 1 ? in_rows * pitch : 0;  // d_in holds in_copies shifted copies
-    pl.A.in2 = d_in2x;
-    pl.A.P2 = (int32_t)in2_pitch(pl.A.W2);
-    pl.A.out = d_out;
-    const KernelSet &ks = kKernels[pl.sid];
-    if (pl.jit) {
-        int dev = 0;
-        CUDA_TRY(cudaGetDevice(&dev));
-        CUfunction f;
-        std::string err;
-        int rc = g_jit.get(dev, variant == 0 ? pl.kb : pl.ko, &f, nullptr, &err);
-        if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
-        if (variant == 0) {
-            void *args[] = {&pl.A};
-            rc = g_jit.launch(f, pl.grid, pl.block, 0, s, args, &err);
-        } else {
-            CUtensorMap map;
-            rc = encode_tmap(&map, d_in, in_rows, in_cols, pitch, pl);
-            if (rc) return rc;
-            void *args[] = {&map, &pl.A};
-            rc = g_jit.launch(f, pl.grid, pl.block, pl.dyn_smem, s, args, &err);
-        }
-        if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
-        return LMT_OK;
-    }
-    if (variant == 0) {
-        if (pl.u_base > 0)
-            kKernelsG[pl.sid].base[u_index(pl.u_base)]<<<pl.grid, pl.block, 0, s>>>(pl.A);
-        else
-            ks.base<<<pl.grid, pl.block, 0, s>>>(pl.A);
-    } else {
-        CUtensorMap map;
-        int rc = encode_tmap(&map, d_in, in_rows, in_cols, pitch, pl);
+// A variant ready to launch: the kernel resolved and loaded, its arguments
+// (and, optimized, the TMA descriptor) built -- everything the host does
+// before a launch, kept outside the timed window.
+struct Ready {
+    CUfunction f = nullptr;
+    SynthArgs A;
+    CUtensorMap map;
+    size_t smem = 0;
+    bool opt = false;
+    JitKey got;
+};
+
+// d_in holds pl.in_copies shifted copies (copy stride in_rows * pitch)
+// when the baseline reads 128-bit rows; d_in2x is in2 in the wrapped-halo
+// layout (k_in2_halo), pitch in2_pitch(in_w).
+int ready_variant(const Plan &pl, int variant, int device, CUcontext ctx, const float *d_in, int64_t in_rows,
+                  int64_t in_cols, int64_t pitch, const float *d_in2x, float *d_out, Ready *r) {
+    r->A = pl.A;
+    r->A.in = d_in;
+    r->A.in_copy = (variant == 0 && pl.in_copies > 1) ? in_rows * pitch : 0;
+    r->A.in2 = d_in2x;
+    r->A.P2 = (int32_t)in2_pitch(pl.A.W2);
+    r->A.out = d_out;
+    r->opt = variant == 1;
+    std::string err;
+    int rc = g_jit.get(device, variant == 0 ? pl.kb : pl.ko, &r->f, &r->got, &err);
+    if (!rc) rc = g_jit.load_in(ctx, r->f, &err);  // no lazy load inside a timed window
+    if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
+    if (r->opt) {
+        rc = encode_tmap(&r->map, d_in, in_rows, in_cols, pitch, pl);
         if (rc) return rc;
-        if (pl.u_opt > 0)
-            kKernelsG[pl.sid].opt[u_index(pl.u_opt)]<<<pl.grid, pl.block, pl.dyn_smem, s>>>(map, pl.A);
-        else
-            (pl.wide ? ks.opt_wide : ks.opt)<<<pl.grid, pl.block, pl.dyn_smem, s>>>(map, pl.A);
+        r->smem = pl.dyn_smem;
     }
-    CUDA_TRY(cudaGetLastError());
     return LMT_OK;
 }
 
+int launch_ready(Ready &r, const Plan &pl, cudaStream_t s) {
+    std::string err;
+    int rc;
+    if (!r.opt) {
+        void *args[] = {&r.A};
+        rc = g_jit.launch(r.f, pl.grid, pl.block, 0, s, args, &err);
+    } else {
+        void *args[] = {&r.map, &r.A};
+        rc = g_jit.launch(r.f, pl.grid, pl.block, r.smem, s, args, &err);
+    }
+    if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
+    return LMT_OK;
+}
 
-int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int sms) {
+int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int blocks_cap) {
     const int64_t total = (h + kIn2PhysHaloRows) * in2_pitch(w);
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, blocks_cap));
     k_in2_halo<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w));
     CUDA_TRY(cudaGetLastError());
     k_in2_shift<<<(unsigned)blocks, 256, 0, s>>>(buf, (int)h, (int)w, (int)in2_pitch(w),
@@ -789,30 +820,459 @@ int launch_in2_halo(float *buf, int64_t h, int64_t w, cudaStream_t s, int sms) {
     return LMT_OK;
 }
 
-int launch_in_shift(float *buf, int64_t rows, int64_t pitch, cudaStream_t s, int sms) {
-    const int64_t total = rows * pitch * (kInCopies - 1);
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 16));
-    k_in_shift<<<(unsigned)blocks, 256, 0, s>>>(buf, rows, pitch);
-    CUDA_TRY(cudaGetLastError());
-    return LMT_OK;
-}
-
-int launch_fill(float *d, int64_t rows, int64_t cols, int64_t pitch, uint32_t salt, cudaStream_t s, int sms) {
+int launch_fill(float *d, int64_t rows, int64_t cols, int64_t pitch, uint32_t salt, cudaStream_t s, int blocks_cap) {
     const int64_t vecs = rows * (pitch / 4);
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, (int64_t)sms * 16));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, blocks_cap));
     k_fill<<<(unsigned)blocks, 256, 0, s>>>(d, rows, cols, pitch, salt);
     CUDA_TRY(cudaGetLastError());
     return LMT_OK;
 }
 
-int launch_digest(const float *a, const float *b, int64_t count, unsigned long long *res, cudaStream_t s, int sms) {
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)sms * 8));
+int launch_digest(const float *a, const float *b, int64_t count, unsigned long long *res, cudaStream_t s,
+                  int blocks_cap) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, blocks_cap));
     k_digest<<<(unsigned)blocks, 256, 0, s>>>(a, b, count, res);
     CUDA_TRY(cudaGetLastError());
     return LMT_OK;
 }
 
 lmt_device dev_or_default(const lmt_device *d) { return d ? *d : kDefaultDevice; }
+
+// ------------------------------------------------------ measurement engine
+
+struct Batch {
+    const lmt_instance *insts;
+    int64_t n;
+    lmt_device d;
+    int32_t flags;
+    int samples;
+    const int64_t *sample_idx;
+    float *sample_vals;
+    const float *const *h_in;
+    const int64_t *h_rows, *h_cols;
+    const float *const *h_in2;
+    float *const *h_ob, *const *h_oo;
+    lmt_measurement *out;
+    std::vector<Plan> plans;
+    std::vector<char> ok, ran_base, ran_opt, filled;
+    bool host() const { return h_in != nullptr; }
+};
+
+bool run_opt_of(const Batch &B, const Plan &pl, const DevCtx *c) {
+    return !(B.flags & LMT_MEASURE_SKIP_OPT) &&
+           (pl.feasible || ((B.flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
+                            (int64_t)pl.A.stage_bytes <= (int64_t)c->smem_optin - 1024));
+}
+
+// The lane's own `in` buffer: host mode holds the copied `in` (and its
+// shifted copies); device mode only the baseline's shifted copies of the
+// shared `in` (0 when the baseline reads the shared one directly).
+size_t need_in_elems(const Batch &B, int64_t i, const Plan &pl) {
+    const int64_t rows = B.host() ? B.h_rows[i] : pl.g.alloc_h;
+    const int64_t cols = B.host() ? B.h_cols[i] : pl.g.alloc_w;
+    if (!B.host() && pl.in_copies == 1) return 0;
+    return (size_t)(rows * round_up(cols, 4)) * pl.in_copies + 64;
+}
+
+// Enqueue instance i on lane L: its inputs, both variants each bracketed by
+// its own events (in alternating order), digest + comparison, sampled cells,
+// and (host mode) the copies. Stream-ordered on L.s; never blocks unless a
+// buffer has to grow.
+int enqueue(DevCtx *c, Batch &B, Lane &L, int64_t i) {
+    const lmt_instance &p = B.insts[i];
+    const Plan &pl = B.plans[(size_t)i];
+    lmt_measurement &m = B.out[i];
+    cudaStream_t s = L.s;
+    const bool whole = L.sms == 0;
+    const int cap_blocks = (whole ? c->sms : L.sms) * 8;
+    cudaEvent_t *ev = &c->events[(size_t)i * kEvPerInst];
+    const int64_t rows = B.host() ? B.h_rows[i] : pl.g.alloc_h;
+    const int64_t cols = B.host() ? B.h_cols[i] : pl.g.alloc_w;
+    const int64_t pitch = round_up(cols, 4);
+    const size_t need_in = need_in_elems(B, i, pl), need_out = (size_t)p.out_h * p.out_w;
+    const bool ropt = run_opt_of(B, pl, c);
+    const bool pipelined = whole && B.host();  // copies on their own streams, two buffer sets
+    const int b = pipelined ? (int)(i & 1) : 0;
+    int rc;
+    if (pipelined && (rc = lane_streams(L))) return rc;
+    // ---- buffers (growing one waits for everything in flight on the lane)
+    if (need_in > L.in_cap[b] || need_out > L.out_cap[b] ||
+        (B.host() && in2_phys_elems(p.in_h, p.in_w) > L.in2_cap[b])) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (L.h2d) {
+            CUDA_TRY(cudaStreamSynchronize(L.h2d));
+            CUDA_TRY(cudaStreamSynchronize(L.d2h));
+        }
+        if (need_in > L.in_cap[b]) {
+            size_t fr = 0, tot = 0;
+            CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+            if (need_in * 4 + ((size_t)256 << 20) > fr + L.in_cap[b] * 4)
+                return fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i, need_in * 4);
+            if ((rc = ensure(&L.in[b], &L.in_cap[b], need_in))) return rc;
+        }
+        if (need_out > L.out_cap[b]) {
+            size_t oc = L.out_cap[b];
+            if ((rc = ensure(&L.ob[b], &oc, need_out))) return rc;
+            oc = L.out_cap[b];
+            if ((rc = ensure(&L.oo[b], &oc, need_out))) return rc;
+            L.out_cap[b] = oc;
+        }
+        if (B.host() && (rc = ensure(&L.in2[b], &L.in2_cap[b], in2_phys_elems(p.in_h, p.in_w)))) return rc;
+    }
+    float *dob = L.ob[b], *doo = L.oo[b];
+    // din: the `in` the optimized variant (and a scalar baseline) reads;
+    // dcp: the baseline's 128-bit layout (4 shifted copies) when it uses one
+    const float *din = nullptr, *din2 = nullptr;
+    float *dcp = pl.in_copies > 1 ? L.in[b] : nullptr;
+    // ---- inputs (make_inputs, interp.py:30-38)
+    if (B.host()) {
+        float *dst = L.in[b];
+        cudaStream_t cs = pipelined ? L.h2d : s;
+        if (pipelined) CUDA_TRY(cudaStreamWaitEvent(cs, L.consumed[b], 0));  // instance i - 2 done with slot b
+        CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)pitch * 4, B.h_in[i], (size_t)cols * 4, (size_t)cols * 4,
+                                   (size_t)rows, cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaMemcpy2DAsync(L.in2[b], (size_t)in2_pitch(p.in_w) * 4, B.h_in2[i], (size_t)p.in_w * 4,
+                                   (size_t)p.in_w * 4, (size_t)p.in_h, cudaMemcpyHostToDevice, cs));
+        if (pipelined) {
+            CUDA_TRY(cudaEventRecord(L.copied[b], cs));
+            CUDA_TRY(cudaStreamWaitEvent(s, L.copied[b], 0));
+        }
+        CUDA_TRY(cudaEventRecord(ev[5], s));
+        if ((rc = launch_in2_halo(L.in2[b], p.in_h, p.in_w, s, cap_blocks))) return rc;
+        CUDA_TRY(cudaEventRecord(ev[6], s));
+        m.launches += 2;
+        B.filled[(size_t)i] = 1;
+        if (pipelined) CUDA_TRY(cudaStreamWaitEvent(s, L.drained[b], 0));  // outs of i - 2 reached the host
+        din = dst;
+        din2 = L.in2[b];
+    } else {  // the shared inputs, generated for the whole batch before it started
+        din = c->ins.at(cols).p;
+        din2 = c->in2s.at({p.in_h, p.in_w});
+    }
+    m.in_copies = pl.in_copies;
+    // ---- both variants, resolved before any event is recorded
+    Ready rb, ro;
+    if ((rc = ready_variant(pl, 0, c->device, L.ctx, dcp ? dcp : din, rows, cols, pitch, din2, dob, &rb))) return rc;
+    if (ropt && (rc = ready_variant(pl, 1, c->device, L.ctx, din, rows, cols, pitch, din2, doo, &ro))) return rc;
+    m.kernel_id = jit_kid(rb.got, ropt ? ro.got : pl.ko);
+    m.lane_sms = L.sms;
+    m.order = (ropt && (i & 1)) ? 1 : 0;
+    const bool flush = whole && !(B.flags & LMT_MEASURE_WARM_L2);
+    // an idle lane would start timing before the host has enqueued the
+    // kernel: give the GPU a short head start first
+    if (!flush && L.inflight.empty() && !B.filled[(size_t)i]) {
+        k_lead<<<1, 32, 0, s>>>(20000ll);
+        CUDA_TRY(cudaGetLastError());
+    }
+    for (int k = 0; k < 2; k++) {
+        const int variant = (k == 0) == (m.order == 0) ? 0 : 1;
+        if (variant == 1 && !ropt) continue;
+        if (flush) {
+            c->scrub_tag += 1.0f;
+            k_scrub<<<c->sms * 4, 256, 0, s>>>(c->scrub, c->scrub_n4, c->scrub_tag);
+            CUDA_TRY(cudaGetLastError());
+            m.launches += 1;
+        }
+        CUDA_TRY(cudaEventRecord(ev[variant * 2], s));
+        if (variant == 0 && dcp) {  // the baseline's own layout, inside its window
+            const int blocks = (int)std::max<int64_t>(
+                1, std::min<int64_t>((rows * pitch * kInCopies + 255) / 256, (whole ? c->sms : L.sms) * 16));
+            if (B.host()) {
+                k_in_shift<<<blocks, 256, 0, s>>>(dcp, rows, pitch);
+            } else {
+                k_in_copy4<<<blocks, 256, 0, s>>>(din, dcp, rows, pitch);
+            }
+            CUDA_TRY(cudaGetLastError());
+            m.launches += 1;
+        }
+        if ((rc = launch_ready(variant == 0 ? rb : ro, pl, s))) return rc;
+        CUDA_TRY(cudaEventRecord(ev[variant * 2 + 1], s));
+        m.launches += 1;
+        (variant == 0 ? B.ran_base : B.ran_opt)[(size_t)i] = 1;
+    }
+    if (!ropt && !pl.feasible) m.status = LMT_ERR_INFEASIBLE;
+    m.nstages = pl.A.nstages;
+    if ((rc = launch_digest(dob, ropt ? doo : nullptr, (int64_t)need_out, c->dres + i * 3, s, cap_blocks))) return rc;
+    m.launches += 1;
+    if (B.samples > 0) {
+        k_gather<<<1, 256, 0, s>>>(dob, ropt ? doo : nullptr, c->didx + i * B.samples, B.samples,
+                                   c->dsamp + i * B.samples * 2);
+        CUDA_TRY(cudaGetLastError());
+        m.launches += 1;
+    }
+    if (B.host()) {
+        cudaStream_t cs = s;
+        if (pipelined) {
+            CUDA_TRY(cudaEventRecord(L.consumed[b], s));
+            CUDA_TRY(cudaStreamWaitEvent(L.d2h, L.consumed[b], 0));
+            cs = L.d2h;
+        }
+        if (B.h_ob && B.h_ob[i]) CUDA_TRY(cudaMemcpyAsync(B.h_ob[i], dob, need_out * 4, cudaMemcpyDeviceToHost, cs));
+        if (ropt && B.h_oo && B.h_oo[i])
+            CUDA_TRY(cudaMemcpyAsync(B.h_oo[i], doo, need_out * 4, cudaMemcpyDeviceToHost, cs));
+        if (pipelined) CUDA_TRY(cudaEventRecord(L.drained[b], cs));
+    }
+    CUDA_TRY(cudaEventRecord(ev[4], s));
+    L.inflight.push_back(i);
+    return LMT_OK;
+}
+
+// Device-generated inputs shared read-only by every lane (make_inputs,
+// interp.py:30-38): in2 (salt 1) per shape in the kernels' wrapped-halo
+// layout, and `in` (salt 0) per logical width with the most rows any
+// instance needs -- hash(r * alloc_w + c) does not depend on the instance
+// otherwise. Generated on the library stream before a batch's kernels;
+// widths unused for the longest are evicted past kSharedInBudget.
+constexpr size_t kSharedInBudget = (size_t)48 << 30;
+
+int ensure_shared_in2(DevCtx *c, int64_t h, int64_t w) {
+    if (c->in2s.count({h, w})) return LMT_OK;
+    float *p = nullptr;
+    size_t cap = 0;
+    int rc;
+    if ((rc = ensure(&p, &cap, in2_phys_elems(h, w)))) return rc;
+    if ((rc = launch_fill(p, h, w, in2_pitch(w), 1, c->stream, c->sms * 8))) return rc;
+    if ((rc = launch_in2_halo(p, h, w, c->stream, c->sms * 8))) return rc;
+    c->in2s[{h, w}] = p;
+    return LMT_OK;
+}
+
+int ensure_shared_ins(DevCtx *c, const std::map<int64_t, int64_t> &need) {
+    c->batch_no++;
+    for (auto &kv : need) {
+        auto it = c->ins.find(kv.first);
+        if (it != c->ins.end() && it->second.rows >= kv.second) { it->second.used = c->batch_no; continue; }
+        const int64_t pitch = round_up(kv.first, 4);
+        const size_t bytes = (size_t)kv.second * pitch * 4;
+        CUDA_TRY(cudaDeviceSynchronize());  // no lane still reads what gets replaced or evicted
+        if (it != c->ins.end()) {
+            CUDA_TRY(cudaFree(it->second.p));
+            c->ins_bytes -= (size_t)it->second.rows * it->second.pitch * 4;
+            c->ins.erase(it);
+        }
+        while (c->ins_bytes + bytes > kSharedInBudget) {  // least recently used width not in this batch
+            auto victim = c->ins.end();
+            for (auto e = c->ins.begin(); e != c->ins.end(); ++e)
+                if (!need.count(e->first) && (victim == c->ins.end() || e->second.used < victim->second.used))
+                    victim = e;
+            if (victim == c->ins.end()) break;
+            CUDA_TRY(cudaFree(victim->second.p));
+            c->ins_bytes -= (size_t)victim->second.rows * victim->second.pitch * 4;
+            c->ins.erase(victim);
+        }
+        DevCtx::SharedIn e;
+        e.rows = kv.second;
+        e.pitch = pitch;
+        e.used = c->batch_no;
+        CUDA_TRY(cudaMalloc(&e.p, bytes + 256));
+        int rc = launch_fill(e.p, e.rows, kv.first, pitch, 0, c->stream, c->sms * 16);
+        if (rc) return rc;
+        c->ins[kv.first] = e;
+        c->ins_bytes += bytes;
+    }
+    return LMT_OK;
+}
+
+// Lane picks for the concurrent phase: the costliest pending instance that
+// needs this lane's size (too wide for the next smaller lane), else the
+// costliest that fits at all (list scheduling, longest first).
+int64_t pick(std::vector<int64_t> &pending, const Batch &B, int lane_sms, int smaller_sms) {
+    size_t best = pending.size();
+    for (size_t k = 0; k < pending.size(); k++) {
+        const int64_t ct = B.plans[(size_t)pending[k]].ctas;
+        if (ct > lane_sms) continue;
+        if (ct > smaller_sms) { best = k; break; }
+        if (best == pending.size()) best = k;
+    }
+    if (best == pending.size()) return -1;
+    const int64_t i = pending[best];
+    pending.erase(pending.begin() + (long)best);
+    return i;
+}
+
+int retire(DevCtx *c, Lane &L, bool wait) {
+    while (!L.inflight.empty()) {
+        cudaEvent_t done = c->events[(size_t)L.inflight.front() * kEvPerInst + 4];
+        if (wait) {
+            CUDA_TRY(cudaEventSynchronize(done));
+        } else {
+            cudaError_t q = cudaEventQuery(done);
+            if (q == cudaErrorNotReady) break;
+            if (q != cudaSuccess) return fail(LMT_ERR_CUDA, "instance failed: %s", cudaGetErrorString(q));
+        }
+        L.inflight.erase(L.inflight.begin());
+    }
+    return LMT_OK;
+}
+
+int measure_run(Batch &B);
+
+// An aborted batch still leaves every record defined: the instances that
+// did not run carry the error.
+int measure_impl(Batch &B) {
+    const int rc = measure_run(B);
+    if (rc != LMT_OK && B.out)
+        for (int64_t i = 0; i < B.n; i++)
+            if (i >= (int64_t)B.ran_base.size() || !B.ran_base[(size_t)i])
+                if (B.out[i].status == LMT_OK) B.out[i].status = rc;
+    return rc;
+}
+
+int measure_run(Batch &B) {
+    if (!B.insts || !B.out || B.n < 0) return fail(LMT_ERR_ARG, "bad measure arguments");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    const int64_t n = B.n;
+    for (int64_t i = 0; i < n; i++) {  // every record defined, whatever happens later
+        memset(&B.out[i], 0, sizeof(lmt_measurement));
+        B.out[i].t_opt_ms = -1.0;
+        B.out[i].mismatches = -1;
+        B.out[i].status = LMT_ERR_CUDA;
+    }
+    B.plans.assign((size_t)n, Plan{});
+    B.ok.assign((size_t)n, 0);
+    B.ran_base.assign((size_t)n, 0);
+    B.ran_opt.assign((size_t)n, 0);
+    B.filled.assign((size_t)n, 0);
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    if ((rc = ensure(&c->dres, &c->dres_cap, nn * 3))) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->dres, 0, nn * 3 * sizeof(unsigned long long), c->stream));
+    if (B.samples > 0) {
+        if ((rc = ensure(&c->didx, &c->didx_cap, nn * B.samples))) return rc;
+        if ((rc = ensure(&c->dsamp, &c->dsamp_cap, nn * B.samples * 2))) return rc;
+    }
+    while (c->events.size() < (size_t)n * kEvPerInst) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        c->events.push_back(e);
+    }
+    if (!(B.flags & LMT_MEASURE_WARM_L2) && !c->scrub) {
+        size_t cap = 0;
+        if ((rc = ensure(&c->scrub, &cap, (size_t)(kScrubBytes / 16)))) return rc;
+        c->scrub_n4 = kScrubBytes / 16;
+    }
+    // ---- plans; the shared in2
+    for (int64_t i = 0; i < n; i++) {
+        const lmt_instance &p = B.insts[i];
+        lmt_geometry g0;
+        std::vector<std::string> v = violations(p);
+        if (!v.empty()) {
+            std::string msg;
+            for (size_t k = 0; k < v.size(); k++) msg += (k ? "; " : "") + v[k];
+            B.out[i].status = fail(LMT_ERR_INVALID_INSTANCE, "%s", msg.c_str());
+            continue;
+        }
+        if ((rc = compute_geometry(p, B.d, &g0))) { B.out[i].status = rc; continue; }
+        const int64_t cols = B.host() ? B.h_cols[i] : g0.alloc_w;
+        Plan &pl = B.plans[(size_t)i];
+        if ((rc = make_plan(p, B.d, round_up(cols, 4), B.flags, c, &pl))) { B.out[i].status = rc; continue; }
+        if (B.host() && (B.h_rows[i] < pl.g.alloc_h || B.h_cols[i] < pl.g.alloc_w)) {
+            B.out[i].status = fail(LMT_ERR_ARG, "instance %lld: in too small", (long long)i);
+            continue;
+        }
+        B.out[i].status = LMT_OK;
+        B.out[i].alg_bytes = pl.alg_bytes;
+        B.out[i].alg_flops = pl.alg_flops;
+        B.out[i].ctas = (int32_t)pl.ctas;
+        B.ok[(size_t)i] = 1;
+        if (!B.host() && (rc = ensure_shared_in2(c, p.in_h, p.in_w))) return rc;
+    }
+    if (!B.host()) {  // the shared `in` of every width the batch reads
+        std::map<int64_t, int64_t> need;
+        for (int64_t i = 0; i < n; i++)
+            if (B.ok[(size_t)i]) {
+                const Plan &pl = B.plans[(size_t)i];
+                int64_t &r = need[pl.g.alloc_w];
+                r = std::max<int64_t>(r, pl.g.alloc_h);
+            }
+        if ((rc = ensure_shared_ins(c, need))) return rc;
+    }
+    CUDA_TRY(cudaEventRecord(c->inputs_ready, c->stream));
+    if (B.samples > 0)
+        CUDA_TRY(cudaMemcpyAsync(c->didx, B.sample_idx, (size_t)n * B.samples * 8, cudaMemcpyHostToDevice,
+                                 c->stream));
+    // ---- placement: partitions for launches that fit one, the whole device otherwise
+    const bool conc = (B.flags & LMT_MEASURE_CONCURRENT) != 0;
+    if (conc && (rc = ensure_parts(c))) return rc;
+    const int max_part = (conc && !c->parts.empty()) ? c->parts.front().sms : 0;
+    std::vector<int64_t> iso, pending;
+    for (int64_t i = 0; i < n; i++) {
+        if (!B.ok[(size_t)i]) continue;
+        const Plan &pl = B.plans[(size_t)i];
+        // a partition lane keeps its own `in`; bound that memory
+        const bool fits = pl.ctas <= max_part && need_in_elems(B, i, pl) * 4 <= ((size_t)6 << 30);
+        (fits ? pending : iso).push_back(i);
+    }
+    auto by_cost = [&](int64_t a, int64_t b) { return B.plans[(size_t)a].est_s > B.plans[(size_t)b].est_s; };
+    std::stable_sort(pending.begin(), pending.end(), by_cost);
+    auto mark_fail = [&](int64_t i, int code) { B.out[i].status = code; B.ok[(size_t)i] = 0; };
+    // phase 1: whole-device instances, one at a time, L2 flushed per variant
+    for (int64_t i : iso) {
+        rc = enqueue(c, B, c->full, i);
+        if (rc == LMT_ERR_CUDA) return rc;
+        if (rc) mark_fail(i, rc);
+        if ((rc = retire(c, c->full, false))) return rc;
+    }
+    if (!pending.empty()) {
+        if ((rc = retire(c, c->full, true))) return rc;
+        if (B.host() && c->full.d2h) CUDA_TRY(cudaStreamSynchronize(c->full.d2h));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+    // phase 2: partitions, list-scheduled, two instances in flight per lane
+    for (Lane &L : c->parts) CUDA_TRY(cudaStreamWaitEvent(L.s, c->inputs_ready, 0));
+    while (!pending.empty()) {
+        bool progressed = false;
+        for (size_t l = c->parts.size(); l-- > 0;) {  // smallest lanes choose first
+            Lane &L = c->parts[l];
+            if ((rc = retire(c, L, false))) return rc;
+            const int smaller = l + 1 < c->parts.size() ? c->parts[l + 1].sms : 0;
+            while (L.inflight.size() < 2) {
+                const int64_t i = pick(pending, B, L.sms, smaller);
+                if (i < 0) break;
+                rc = enqueue(c, B, L, i);
+                if (rc == LMT_ERR_CUDA) return rc;
+                if (rc) mark_fail(i, rc);
+                progressed = true;
+            }
+        }
+        if (!progressed) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    for (Lane &L : c->parts)
+        if ((rc = retire(c, L, true))) return rc;
+    if ((rc = retire(c, c->full, true))) return rc;
+    if (c->full.d2h) CUDA_TRY(cudaStreamSynchronize(c->full.d2h));
+    // ---- results
+    std::vector<unsigned long long> res(nn * 3);
+    CUDA_TRY(cudaMemcpyAsync(res.data(), c->dres, res.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             c->stream));
+    if (B.samples > 0)
+        CUDA_TRY(cudaMemcpyAsync(B.sample_vals, c->dsamp, (size_t)n * B.samples * 2 * sizeof(float),
+                                 cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; i++) {
+        lmt_measurement &m = B.out[i];
+        cudaEvent_t *ev = &c->events[(size_t)i * kEvPerInst];
+        float ms = 0.0f;
+        if (B.ran_base[(size_t)i]) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+            m.t_base_ms = ms;
+            m.digest_base = res[(size_t)i * 3];
+        }
+        if (B.filled[(size_t)i]) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, ev[5], ev[6]));
+            m.t_fill_ms = ms;
+        }
+        if (B.ran_opt[(size_t)i]) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+            m.t_opt_ms = ms;
+            m.digest_opt = res[(size_t)i * 3 + 1];
+            m.mismatches = (int64_t)res[(size_t)i * 3 + 2];
+        }
+    }
+    return LMT_OK;
+}
 
 }  // namespace
 
@@ -845,23 +1305,23 @@ int lmt_fill(float *d_dst, int64_t rows, int64_t cols, int64_t pitch, uint32_t s
     DevCtx *c;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    return launch_fill(d_dst, rows, cols, pitch, salt, (cudaStream_t)stream, c->sms);
+    return launch_fill(d_dst, rows, cols, pitch, salt, (cudaStream_t)stream, c->sms * 16);
 }
 
 int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, const float *d_in, int64_t in_rows,
                 int64_t in_cols, int64_t in_pitch, const float *d_in2, float *d_out, void *stream) {
     if (!inst || !d_in || !d_in2 || !d_out) return fail(LMT_ERR_ARG, "null argument");
     if (variant != 0 && variant != 1) return fail(LMT_ERR_ARG, "variant must be 0 or 1");
-    // the 128-bit row loads and the TMA descriptor need 16-byte rows
-    if (in_pitch % 4 || reinterpret_cast<uintptr_t>(d_in) % 16)
-        return fail(LMT_ERR_ARG, "in pitch must be a multiple of 4 floats and the base 16-byte aligned");
+    // the TMA descriptor needs 16-byte rows; rows must not overlap
+    if (in_pitch < in_cols || in_pitch % 4 || reinterpret_cast<uintptr_t>(d_in) % 16)
+        return fail(LMT_ERR_ARG, "in pitch must be >= in_cols and a multiple of 4 floats, the base 16-byte aligned");
     std::lock_guard<std::mutex> lk(g_mu);
     DevCtx *c;
     int rc = get_ctx(&c);
     if (rc) return rc;
     const lmt_device d = dev_or_default(dev);
     Plan pl;
-    rc = make_plan(*inst, d, in_pitch, &pl, c);
+    rc = make_plan(*inst, d, in_pitch, 0, c, &pl);
     if (rc) return rc;
     if (in_rows < pl.g.alloc_h || in_cols < pl.g.alloc_w)
         return fail(LMT_ERR_ARG, "in is %lldx%lld, instance needs %lldx%lld", (long long)in_rows, (long long)in_cols,
@@ -871,24 +1331,23 @@ int lmt_execute(const lmt_instance *inst, const lmt_device *dev, int variant, co
     if (variant == 1 && (int64_t)pl.A.stage_bytes > (int64_t)c->smem_optin - 1024)
         return fail(LMT_ERR_INFEASIBLE, "local-memory footprint %lld bytes exceeds capacity %d",
                     (long long)pl.g.footprint_bytes, (int)c->smem_optin - 1024);
+    // the caller's `in` is read as is: the baseline uses scalar stencil loads here
+    pl.kb.vec = 0;
+    pl.in_copies = 1;
     // stage the caller's in2 into the wrapped-halo layout (stream-ordered scratch)
     cudaStream_t s = (cudaStream_t)stream;
     float *x = nullptr;
     CUDA_TRY(cudaMallocAsync(&x, in2_phys_elems(inst->in_h, inst->in_w) * sizeof(float), s));
-    CUDA_TRY(cudaMemcpy2DAsync(x, (size_t)in2_pitch(inst->in_w) * 4, d_in2, (size_t)inst->in_w * 4,
-                               (size_t)inst->in_w * 4, (size_t)inst->in_h, cudaMemcpyDeviceToDevice, s));
-    rc = launch_in2_halo(x, inst->in_h, inst->in_w, s, c->sms);
-    // the baseline's 128-bit row loads read shifted copies of `in`: stage them too
-    float *xin = nullptr;
-    if (rc == LMT_OK && variant == 0 && pl.in_copies > 1) {
-        const size_t n = (size_t)in_rows * (size_t)in_pitch;
-        CUDA_TRY(cudaMallocAsync(&xin, (n * pl.in_copies + 64) * sizeof(float), s));
-        CUDA_TRY(cudaMemcpyAsync(xin, d_in, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
-        rc = launch_in_shift(xin, in_rows, in_pitch, s, c->sms);
-    }
-    if (rc == LMT_OK) rc = launch_variant(pl, variant, xin ? xin : d_in, in_rows, in_cols, in_pitch, x, d_out, s);
-    if (xin) CUDA_TRY(cudaFreeAsync(xin, s));
-    CUDA_TRY(cudaFreeAsync(x, s));
+    rc = LMT_OK;
+    cudaError_t ce = cudaMemcpy2DAsync(x, (size_t)in2_pitch(inst->in_w) * 4, d_in2, (size_t)inst->in_w * 4,
+                                       (size_t)inst->in_w * 4, (size_t)inst->in_h, cudaMemcpyDeviceToDevice, s);
+    if (ce != cudaSuccess) rc = fail(LMT_ERR_CUDA, "in2 staging: %s", cudaGetErrorString(ce));
+    if (rc == LMT_OK) rc = launch_in2_halo(x, inst->in_h, inst->in_w, s, c->sms * 8);
+    Ready r;
+    if (rc == LMT_OK) rc = ready_variant(pl, variant, c->device, nullptr, d_in, in_rows, in_cols, in_pitch, x, d_out, &r);
+    if (rc == LMT_OK) rc = launch_ready(r, pl, s);
+    ce = cudaFreeAsync(x, s);
+    if (rc == LMT_OK && ce != cudaSuccess) rc = fail(LMT_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(ce));
     return rc;
 }
 
@@ -899,250 +1358,57 @@ int lmt_digest(const float *d, int64_t count, uint64_t *h_out, void *stream) {
     int rc = get_ctx(&c);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    rc = ensure(&c->dres, &c->dres_cap, 3);
+    unsigned long long *res = nullptr;
+    CUDA_TRY(cudaMallocAsync(&res, 3 * sizeof(unsigned long long), s));
+    unsigned long long h[3] = {0, 0, 0};
+    cudaError_t e = cudaMemsetAsync(res, 0, 3 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) rc = launch_digest(d, nullptr, count, res, s, c->sms * 8);
+    if (e == cudaSuccess && rc == LMT_OK) e = cudaMemcpyAsync(h, res, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(res, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(LMT_ERR_CUDA, "digest: %s", cudaGetErrorString(e));
     if (rc) return rc;
-    CUDA_TRY(cudaMemsetAsync(c->dres, 0, 3 * sizeof(unsigned long long), s));
-    rc = launch_digest(d, nullptr, count, c->dres, s, c->sms);
-    if (rc) return rc;
-    unsigned long long h[3];
-    CUDA_TRY(cudaMemcpyAsync(h, c->dres, sizeof h, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
     *h_out = h[0];
     return LMT_OK;
 }
 
-static int measure_impl(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
-                        const float *const *h_in, const int64_t *h_rows, const int64_t *h_cols,
-                        const float *const *h_in2, float *const *h_ob, float *const *h_oo, lmt_measurement *out) {
-    if (!insts || !out || n < 0) return fail(LMT_ERR_ARG, "bad measure arguments");
-    std::lock_guard<std::mutex> lk(g_mu);
-    DevCtx *c;
-    int rc = get_ctx(&c);
-    if (rc) return rc;
-    const lmt_device d = dev_or_default(dev);
-    cudaStream_t s = c->stream;
-    const bool host = h_in != nullptr;
-    rc = ensure(&c->dres, &c->dres_cap, (size_t)std::max<int64_t>(n, 1) * 3);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemsetAsync(c->dres, 0, (size_t)std::max<int64_t>(n, 1) * 3 * sizeof(unsigned long long), s));
-    const size_t nev = (size_t)n * 4;
-    while (c->events.size() < nev) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreate(&e));
-        c->events.push_back(e);
-    }
-    std::vector<char> ran_base((size_t)n, 0), ran_opt((size_t)n, 0), filled((size_t)n, 0);
-    for (int64_t i = 0; i < n; i++) {
-        lmt_measurement &m = out[i];
-        memset(&m, 0, sizeof m);
-        m.t_opt_ms = -1.0;
-        m.mismatches = -1;
-        const lmt_instance &p = insts[i];
-        // physical pitch: the logical pitch rounded to 16 bytes (TMA stride rule)
-        lmt_geometry g0;
-        int grc = LMT_OK;
-        {
-            std::vector<std::string> v = violations(p);
-            if (!v.empty()) {
-                std::string msg;
-                for (size_t k = 0; k < v.size(); k++) msg += (k ? "; " : "") + v[k];
-                m.status = fail(LMT_ERR_INVALID_INSTANCE, "%s", msg.c_str());
-                continue;
+int lmt_measure_batch_ex(const lmt_instance *insts, int64_t n, const lmt_device *dev, const lmt_measure_opts *opts,
+                         const float *const *h_in, const int64_t *in_rows, const int64_t *in_cols,
+                         const float *const *h_in2, float *const *h_out_base, float *const *h_out_opt,
+                         lmt_measurement *out) {
+    if (h_in && (!in_rows || !in_cols || !h_in2)) return fail(LMT_ERR_ARG, "host inputs need rows, cols and in2");
+    if (opts && opts->samples > 0 && (!opts->sample_idx || !opts->h_sample_vals))
+        return fail(LMT_ERR_ARG, "samples need sample_idx and h_sample_vals");
+    if (opts && opts->samples > 0 && opts->sample_idx)
+        for (int64_t i = 0; i < n; i++)
+            for (int k = 0; k < opts->samples; k++) {
+                const int64_t v = opts->sample_idx[i * opts->samples + k];
+                if (v < 0 || v >= (int64_t)insts[i].out_h * insts[i].out_w)
+                    return fail(LMT_ERR_ARG, "sample index %lld out of range for instance %lld", (long long)v,
+                                (long long)i);
             }
-            grc = compute_geometry(p, d, &g0);
-            if (grc) { m.status = grc; continue; }
-        }
-        const int64_t rows = host ? h_rows[i] : g0.alloc_h;
-        const int64_t cols = host ? h_cols[i] : g0.alloc_w;
-        const int64_t pitch = round_up(cols, 4);
-        Plan pl;
-        rc = make_plan(p, d, pitch, &pl, c);
-        if (rc) { m.status = rc; continue; }
-        if (rows < pl.g.alloc_h || cols < pl.g.alloc_w) {
-            m.status = fail(LMT_ERR_ARG, "instance %lld: in too small", (long long)i);
-            continue;
-        }
-        m.alg_bytes = pl.alg_bytes;
-        m.alg_flops = pl.alg_flops;
-        m.kernel_id = pl.jit ? jit_kid(pl.kb, pl.ko)
-                             : pl.sid * 100 + (pl.wide ? 50 : 0) + pl.u_base * 10 + pl.u_opt;
-        cudaEvent_t *ev = &c->events[(size_t)i * 4];
-        // ---- inputs (make_inputs, interp.py:30-38)
-        const size_t need_in = (size_t)(rows * pitch) * pl.in_copies + 64, need_out = (size_t)p.out_h * p.out_w;
-        const size_t need_in2 = in2_phys_elems(p.in_h, p.in_w);
-        const int64_t p2 = in2_pitch(p.in_w);
-        float *din, *din2, *dob, *doo;
-        const int b = (int)(i & 1);
-        if (host) {
-            // slot b was last used by instance i - 2: its buffers grow only with every stream idle
-            if (need_in > c->hin_cap[b] || need_in2 > c->hin2_cap[b] || need_out > c->hob_cap[b] ||
-                need_out > c->hoo_cap[b]) {
-                CUDA_TRY(cudaStreamSynchronize(s));
-                CUDA_TRY(cudaStreamSynchronize(c->h2d));
-                CUDA_TRY(cudaStreamSynchronize(c->d2h));
-                if (need_in > c->hin_cap[b]) {
-                    size_t fr = 0, tot = 0;
-                    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-                    if (need_in * 4 + ((size_t)256 << 20) > fr + c->hin_cap[b] * 4) {
-                        m.status = fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i,
-                                        need_in * 4);
-                        continue;
-                    }
-                }
-                if ((rc = ensure(&c->hin[b], &c->hin_cap[b], need_in)) ||
-                    (rc = ensure(&c->hin2[b], &c->hin2_cap[b], need_in2)) ||
-                    (rc = ensure(&c->hob[b], &c->hob_cap[b], need_out)) ||
-                    (rc = ensure(&c->hoo[b], &c->hoo_cap[b], need_out)))
-                    return rc;
-            }
-            din = c->hin[b];
-            din2 = c->hin2[b];
-            dob = c->hob[b];
-            doo = c->hoo[b];
-            // H2D on its own stream once instance i - 2's kernels are done with the slot
-            CUDA_TRY(cudaStreamWaitEvent(c->h2d, c->consumed[b], 0));
-            CUDA_TRY(cudaMemcpy2DAsync(din, (size_t)pitch * 4, h_in[i], (size_t)cols * 4, (size_t)cols * 4,
-                                       (size_t)rows, cudaMemcpyHostToDevice, c->h2d));
-            CUDA_TRY(cudaMemcpy2DAsync(din2, (size_t)p2 * 4, h_in2[i], (size_t)p.in_w * 4, (size_t)p.in_w * 4,
-                                       (size_t)p.in_h, cudaMemcpyHostToDevice, c->h2d));
-            CUDA_TRY(cudaEventRecord(c->copied[b], c->h2d));
-            CUDA_TRY(cudaStreamWaitEvent(s, c->copied[b], 0));
-            CUDA_TRY(cudaEventRecord(ev[3], s));
-            filled[(size_t)i] = 1;
-            if (pl.in_copies > 1) {
-                rc = launch_in_shift(din, rows, pitch, s, c->sms);
-                if (rc) return rc;
-                m.launches += 1;
-            }
-            rc = launch_in2_halo(din2, p.in_h, p.in_w, s, c->sms);
-            if (rc) return rc;
-            m.launches += 1;
-            // the outputs of slot b must have reached the host (instance i - 2)
-            CUDA_TRY(cudaStreamWaitEvent(s, c->drained[b], 0));
-        } else {
-            if (c->in_rows != rows || c->in_cols != cols || c->in_pitch != pitch || !c->in ||
-                c->in_copies < pl.in_copies) {
-                if (need_in > c->in_cap) {
-                    CUDA_TRY(cudaStreamSynchronize(s));
-                    size_t fr = 0, tot = 0;
-                    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-                    if (need_in * 4 + ((size_t)256 << 20) > fr + c->in_cap * 4) {
-                        m.status = fail(LMT_ERR_TOO_LARGE, "instance %lld: in needs %zu bytes", (long long)i, need_in * 4);
-                        continue;
-                    }
-                    rc = ensure(&c->in, &c->in_cap, need_in);
-                    if (rc) return rc;
-                }
-                CUDA_TRY(cudaEventRecord(ev[3], s));
-                rc = launch_fill(c->in, rows, cols, pitch, 0, s, c->sms);
-                if (rc) return rc;
-                m.launches += 1;
-                if (pl.in_copies > 1) {
-                    rc = launch_in_shift(c->in, rows, pitch, s, c->sms);
-                    if (rc) return rc;
-                    m.launches += 1;
-                }
-                c->in_copies = pl.in_copies;
-                c->in_rows = rows;
-                c->in_cols = cols;
-                c->in_pitch = pitch;
-                filled[(size_t)i] = 1;
-            }
-            if (c->in2_h != p.in_h || c->in2_w != p.in_w || !c->in2) {
-                rc = ensure(&c->in2, &c->in2_cap, need_in2);
-                if (rc) return rc;
-                if (!filled[(size_t)i]) { CUDA_TRY(cudaEventRecord(ev[3], s)); filled[(size_t)i] = 1; }
-                rc = launch_fill(c->in2, p.in_h, p.in_w, p2, 1, s, c->sms);
-                if (rc) return rc;
-                m.launches += 1;
-                rc = launch_in2_halo(c->in2, p.in_h, p.in_w, s, c->sms);
-                if (rc) return rc;
-                m.launches += 1;
-                c->in2_h = p.in_h;
-                c->in2_w = p.in_w;
-            }
-            rc = ensure(&c->outb, &c->outb_cap, need_out);
-            if (rc) return rc;
-            rc = ensure(&c->outo, &c->outo_cap, need_out);
-            if (rc) return rc;
-            din = c->in;
-            din2 = c->in2;
-            dob = c->outb;
-            doo = c->outo;
-        }
-        // ---- K1, K2 timed with events on the launching stream; a kernel not
-        // yet compiled/loaded is resolved first, outside the events
-        if (pl.jit) {
-            std::string err;
-            CUfunction f;
-            JitKey gb = pl.kb, go = pl.ko;
-            int jrc = g_jit.get(c->device, pl.kb, &f, &gb, &err);
-            if (!jrc && !(flags & LMT_MEASURE_SKIP_OPT) && pl.feasible) jrc = g_jit.get(c->device, pl.ko, &f, &go, &err);
-            if (jrc) { m.status = fail(LMT_ERR_CUDA, "%s", err.c_str()); continue; }
-            m.kernel_id = jit_kid(gb, go);  // the kernels built
-        }
-        CUDA_TRY(cudaEventRecord(ev[0], s));
-        rc = launch_variant(pl, 0, din, rows, cols, pitch, din2, dob, s);
-        if (rc) { m.status = rc; continue; }
-        CUDA_TRY(cudaEventRecord(ev[1], s));
-        ran_base[(size_t)i] = 1;
-        m.launches += 1;
-        m.nstages = pl.A.nstages;
-        const bool run_opt = !(flags & LMT_MEASURE_SKIP_OPT) &&
-                             (pl.feasible || ((flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
-                                              (int64_t)pl.A.stage_bytes <= (int64_t)c->smem_optin - 1024));
-        if (run_opt) {
-            rc = launch_variant(pl, 1, din, rows, cols, pitch, din2, doo, s);
-            if (rc) { m.status = rc; continue; }
-            CUDA_TRY(cudaEventRecord(ev[2], s));
-            ran_opt[(size_t)i] = 1;
-            m.launches += 1;
-        } else if (!pl.feasible) {
-            m.status = LMT_ERR_INFEASIBLE;
-        }
-        rc = launch_digest(dob, run_opt ? doo : nullptr, (int64_t)need_out, c->dres + i * 3, s, c->sms);
-        if (rc) return rc;
-        m.launches += 1;
-        if (host) {  // D2H on its own stream, overlapping instance i + 1
-            CUDA_TRY(cudaEventRecord(c->consumed[b], s));
-            CUDA_TRY(cudaStreamWaitEvent(c->d2h, c->consumed[b], 0));
-            if (h_ob && h_ob[i])
-                CUDA_TRY(cudaMemcpyAsync(h_ob[i], dob, need_out * 4, cudaMemcpyDeviceToHost, c->d2h));
-            if (run_opt && h_oo && h_oo[i])
-                CUDA_TRY(cudaMemcpyAsync(h_oo[i], doo, need_out * 4, cudaMemcpyDeviceToHost, c->d2h));
-            CUDA_TRY(cudaEventRecord(c->drained[b], c->d2h));
-        }
-    }
-    if (host) CUDA_TRY(cudaStreamSynchronize(c->d2h));
-    std::vector<unsigned long long> res((size_t)std::max<int64_t>(n, 1) * 3);
-    CUDA_TRY(cudaMemcpyAsync(res.data(), c->dres, res.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    for (int64_t i = 0; i < n; i++) {
-        lmt_measurement &m = out[i];
-        cudaEvent_t *ev = &c->events[(size_t)i * 4];
-        float ms = 0.0f;
-        if (ran_base[(size_t)i]) {
-            CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-            m.t_base_ms = ms;
-            m.digest_base = res[(size_t)i * 3];
-            if (filled[(size_t)i]) {
-                CUDA_TRY(cudaEventElapsedTime(&ms, ev[3], ev[0]));
-                m.t_fill_ms = ms;
-            }
-        }
-        if (ran_opt[(size_t)i]) {
-            CUDA_TRY(cudaEventElapsedTime(&ms, ev[1], ev[2]));
-            m.t_opt_ms = ms;
-            m.digest_opt = res[(size_t)i * 3 + 1];
-            m.mismatches = (int64_t)res[(size_t)i * 3 + 2];
-        }
-    }
-    return LMT_OK;
+    Batch B;
+    B.insts = insts;
+    B.n = n;
+    B.d = dev_or_default(dev);
+    B.flags = opts ? opts->flags : 0;
+    B.samples = opts ? std::max(0, opts->samples) : 0;
+    B.sample_idx = opts ? opts->sample_idx : nullptr;
+    B.sample_vals = opts ? opts->h_sample_vals : nullptr;
+    B.h_in = h_in;
+    B.h_rows = in_rows;
+    B.h_cols = in_cols;
+    B.h_in2 = h_in2;
+    B.h_ob = h_out_base;
+    B.h_oo = h_out_opt;
+    B.out = out;
+    return measure_impl(B);
 }
 
 int lmt_measure_batch(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
                       lmt_measurement *out) {
-    return measure_impl(insts, n, dev, flags, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
+    lmt_measure_opts o{flags, 0, nullptr, nullptr};
+    return lmt_measure_batch_ex(insts, n, dev, &o, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
 }
 
 int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
@@ -1150,7 +1416,20 @@ int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_devic
                            const float *const *h_in2, float *const *h_out_base, float *const *h_out_opt,
                            lmt_measurement *out) {
     if (!h_in || !in_rows || !in_cols || !h_in2) return fail(LMT_ERR_ARG, "host inputs required");
-    return measure_impl(insts, n, dev, flags, h_in, in_rows, in_cols, h_in2, h_out_base, h_out_opt, out);
+    lmt_measure_opts o{flags, 0, nullptr, nullptr};
+    return lmt_measure_batch_ex(insts, n, dev, &o, h_in, in_rows, in_cols, h_in2, h_out_base, h_out_opt, out);
+}
+
+int lmt_partitions(int32_t *sizes, int32_t cap, int32_t *count) {
+    if (!count) return fail(LMT_ERR_ARG, "null argument");
+    std::lock_guard<std::mutex> lk(g_mu);
+    DevCtx *c;
+    int rc = get_ctx(&c);
+    if (rc) return rc;
+    if ((rc = ensure_parts(c))) return rc;
+    *count = (int32_t)c->parts.size();
+    for (int32_t k = 0; sizes && k < cap && k < (int32_t)c->parts.size(); k++) sizes[k] = c->parts[(size_t)k].sms;
+    return LMT_OK;
 }
 
 int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags, int32_t nthreads,
@@ -1164,23 +1443,26 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
         int rc = get_ctx(&c);
         if (rc) return rc;
         device = c->device;
+        if ((flags & LMT_MEASURE_CONCURRENT) && (rc = ensure_parts(c))) return rc;
         const lmt_device d = dev_or_default(dev);
         size_t fr = 0, tot = 0;
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-        size_t max_in = 0, max_in2 = 0, max_out = 0;
+        size_t max_in = 0, max_out = 0;
         for (int64_t i = 0; i < n; i++) {
             const lmt_instance &p = insts[i];
             if (!violations(p).empty()) continue;
             lmt_geometry g0;
             if (compute_geometry(p, d, &g0)) continue;
             Plan pl;
-            if (make_plan(p, d, round_up(g0.alloc_w, 4), &pl, c)) continue;
-            // the device-input buffers the batch will need (measure_impl's sizes)
-            const size_t need_in = (size_t)(g0.alloc_h * round_up(g0.alloc_w, 4)) * pl.in_copies + 64;
-            if (need_in * 4 + ((size_t)1 << 30) <= fr + c->in_cap * 4) max_in = std::max(max_in, need_in);
-            max_in2 = std::max(max_in2, in2_phys_elems(p.in_h, p.in_w));
+            if (make_plan(p, d, round_up(g0.alloc_w, 4), flags, c, &pl)) continue;
+            // the whole-device lane's buffers (measure_impl's sizes): the
+            // baseline's shifted copies, when it reads them
+            const size_t need_in =
+                pl.in_copies > 1 ? (size_t)(g0.alloc_h * round_up(g0.alloc_w, 4)) * pl.in_copies + 64 : 0;
+            if (need_in * 4 + ((size_t)1 << 30) <= fr + c->full.in_cap[0] * 4) max_in = std::max(max_in, need_in);
             max_out = std::max(max_out, (size_t)p.out_h * p.out_w);
-            if (!pl.jit) continue;
+            if (!violations(p).empty() || !p.in_h) continue;
+            if ((rc = ensure_shared_in2(c, p.in_h, p.in_w))) return rc;
             keys.push_back(pl.kb);
             const bool run_opt = !(flags & LMT_MEASURE_SKIP_OPT) &&
                                  (pl.feasible || ((flags & LMT_MEASURE_ALLOW_LARGE_LMEM) &&
@@ -1189,20 +1471,27 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
         }
         // reserve them now: growing a buffer inside a timed batch means a
         // stream sync and a multi-GB cudaFree/cudaMalloc with the GPU idle
-        if (max_in > c->in_cap) {
+        Lane &L = c->full;
+        if (max_in > L.in_cap[0]) {
             CUDA_TRY(cudaStreamSynchronize(c->stream));
-            if ((rc = ensure(&c->in, &c->in_cap, max_in))) return rc;
-            c->in_rows = c->in_cols = c->in_pitch = -1;  // contents no longer valid
+            if ((rc = ensure(&L.in[0], &L.in_cap[0], max_in))) return rc;
         }
-        if (max_in2 > c->in2_cap) {
+        if (max_out > L.out_cap[0]) {
             CUDA_TRY(cudaStreamSynchronize(c->stream));
-            if ((rc = ensure(&c->in2, &c->in2_cap, max_in2))) return rc;
-            c->in2_h = c->in2_w = -1;
+            size_t oc = L.out_cap[0];
+            if ((rc = ensure(&L.ob[0], &oc, max_out))) return rc;
+            oc = L.out_cap[0];
+            if ((rc = ensure(&L.oo[0], &oc, max_out))) return rc;
+            L.out_cap[0] = oc;
         }
-        if (max_out > c->outb_cap || max_out > c->outo_cap) {
-            CUDA_TRY(cudaStreamSynchronize(c->stream));
-            if ((rc = ensure(&c->outb, &c->outb_cap, max_out)) || (rc = ensure(&c->outo, &c->outo_cap, max_out)))
-                return rc;
+        for (Lane &P : c->parts) {  // partition lanes: outputs up front, inputs grow on demand
+            if (max_out > P.out_cap[0]) {
+                size_t oc = P.out_cap[0];
+                if ((rc = ensure(&P.ob[0], &oc, max_out))) return rc;
+                oc = P.out_cap[0];
+                if ((rc = ensure(&P.oo[0], &oc, max_out))) return rc;
+                P.out_cap[0] = oc;
+            }
         }
     }
     std::sort(keys.begin(), keys.end());
@@ -1216,9 +1505,16 @@ int lmt_prepare(const lmt_instance *insts, int64_t n, const lmt_device *dev, int
     }
     int rc = g_jit.prepare(keys, nt, &err);
     if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
-    for (const JitKey &k : keys) {  // load the modules now, not inside a timed batch
+    std::vector<CUcontext> ctxs;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        ctxs.push_back(g_ctx[device].full.ctx);
+        for (const Lane &P : g_ctx[device].parts) ctxs.push_back(P.ctx);
+    }
+    for (const JitKey &k : keys) {  // load the kernels into every context now, not inside a timed batch
         CUfunction f;
         rc = g_jit.get(device, k, &f, nullptr, &err);
+        for (size_t q = 0; !rc && q < ctxs.size(); q++) rc = g_jit.load_in(ctxs[q], f, &err);
         if (rc) return fail(LMT_ERR_CUDA, "%s", err.c_str());
     }
     if (kernels_out) *kernels_out = (int64_t)keys.size();
@@ -1401,17 +1697,6 @@ struct RealBufs {
     unsigned long long *dres = nullptr;
 } g_real[64];
 
-int real_attrs_once(int smem_optin) {
-    static bool done = false;
-    if (done) return LMT_OK;
-    const int cap = smem_optin - 1024;
-    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_opt), cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_rows_opt), cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_cols_opt), cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-    done = true;
-    return LMT_OK;
-}
-
 }  // namespace
 
 int lmt_real_validate(const lmt_real_instance *inst, char *msg, int64_t cap) {
@@ -1430,7 +1715,6 @@ int lmt_real_execute(const lmt_real_instance *inst, int variant, const float *co
     DevCtx *c;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    if ((rc = real_attrs_once((int)c->smem_optin))) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     float *tmp = nullptr;
     if (inst->kernel == 2) CUDA_TRY(cudaMallocAsync(&tmp, (size_t)inst->n * inst->n * 4, s));
@@ -1445,7 +1729,6 @@ int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, l
     DevCtx *c;
     int rc = get_ctx(&c);
     if (rc) return rc;
-    if ((rc = real_attrs_once((int)c->smem_optin))) return rc;
     RealBufs &B = g_real[c->device];
     cudaStream_t s = c->stream;
     std::vector<cudaEvent_t> ev((size_t)n * 3);
@@ -1478,13 +1761,13 @@ int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, l
         // the inputs of this kernel (salts per array; the conv input shares the A buffer slot 0)
         const size_t nn = (size_t)N * N;
         if (r.kernel == 2) {
-            rc = launch_fill(B.in[0], N, N, N, kRealSalt[2], s, c->sms);
+            rc = launch_fill(B.in[0], N, N, N, kRealSalt[2], s, c->sms * 16);
         } else {
-            rc = launch_fill(B.in[0], N, N, N, kRealSalt[0], s, c->sms);
-            if (!rc && r.kernel == 1) rc = launch_fill(B.in[1], N, N, N, kRealSalt[1], s, c->sms);
+            rc = launch_fill(B.in[0], N, N, N, kRealSalt[0], s, c->sms * 16);
+            if (!rc && r.kernel == 1) rc = launch_fill(B.in[1], N, N, N, kRealSalt[1], s, c->sms * 16);
             if (!rc && r.kernel == 3) {
                 for (int k = 0; k < 4 && !rc; k++)
-                    rc = launch_fill(B.in[1 + k], 1, N, (N + 3) / 4 * 4, kRealSalt[3 + k], s, c->sms);
+                    rc = launch_fill(B.in[1 + k], 1, N, (N + 3) / 4 * 4, kRealSalt[3 + k], s, c->sms * 16);
             }
         }
         if (rc) return rc;
@@ -1507,7 +1790,7 @@ int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, l
         const int64_t count = r.kernel == 3 ? 2 * N : (int64_t)nn;
         const size_t slot = (size_t)(i % 4096) * 3;
         CUDA_TRY(cudaMemsetAsync(B.dres + slot, 0, 3 * sizeof(unsigned long long), s));
-        rc = launch_digest(B.ob, run_opt ? B.oo : nullptr, count, B.dres + slot, s, c->sms);
+        rc = launch_digest(B.ob, run_opt ? B.oo : nullptr, count, B.dres + slot, s, c->sms * 8);
         if (rc) return rc;
         CUDA_TRY(cudaMemcpyAsync(&res[(size_t)i * 3], B.dres + slot, 3 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s));
@@ -1562,8 +1845,8 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
     return LMT_OK;
 }
 
-int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, char *buf, int64_t cap,
-                      int64_t *len_out) {
+int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, int32_t flags, char *buf,
+                      int64_t cap, int64_t *len_out) {
     if (!inst || (variant != 0 && variant != 1)) return fail(LMT_ERR_ARG, "bad kernel_source arguments");
     std::lock_guard<std::mutex> lk(g_mu);
     DevCtx *c = nullptr;
@@ -1577,9 +1860,8 @@ int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int varia
         for (auto &v : violations(*inst)) m += (m.empty() ? "" : "; ") + v;
         return fail(LMT_ERR_INVALID_INSTANCE, "%s", m.c_str());
     }
-    rc = make_plan(*inst, d, round_up(g0.alloc_w, 4), &pl, c);
+    rc = make_plan(*inst, d, round_up(g0.alloc_w, 4), flags, c, &pl);
     if (rc) return rc;
-    if (!pl.jit) return fail(LMT_ERR_ARG, "specialised kernels disabled (LMT_JIT=0)");
     const std::string src = (variant == 0 ? pl.kb : pl.ko).defines() + kLmtJitSource;
     if (len_out) *len_out = (int64_t)src.size();
     if (buf && cap > 0) snprintf(buf, (size_t)cap, "%s", src.c_str());
@@ -1711,7 +1993,7 @@ int lmt_rf_mean(const lmt_forest *f, const double *d_X, int64_t nrows, double *d
 }
 
 int lmt_rf_mean_host(const lmt_forest *f, const double *h_X, int64_t nrows, double *h_mean, int32_t *h_votes) {
-    if (!f || nrows < 0) return fail(LMT_ERR_ARG, "bad rf arguments");
+    if (!f || nrows < 0 || (nrows > 0 && (!h_X || !h_mean))) return fail(LMT_ERR_ARG, "bad rf arguments");
     if (nrows == 0) return LMT_OK;
     DevCtx *c;
     {
@@ -1719,20 +2001,32 @@ int lmt_rf_mean_host(const lmt_forest *f, const double *h_X, int64_t nrows, doub
         int rc = get_ctx(&c);
         if (rc) return rc;
     }
+    cudaStream_t s = c->stream;
     double *dX = nullptr, *dm = nullptr;
     int32_t *dv = nullptr;
-    CUDA_TRY(cudaMallocAsync(&dX, (size_t)nrows * f->nfeat * sizeof(double), c->stream));
-    CUDA_TRY(cudaMallocAsync(&dm, (size_t)nrows * sizeof(double), c->stream));
-    if (h_votes) CUDA_TRY(cudaMallocAsync(&dv, (size_t)nrows * sizeof(int32_t), c->stream));
-    CUDA_TRY(cudaMemcpyAsync(dX, h_X, (size_t)nrows * f->nfeat * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    int rc = lmt_rf_mean(f, dX, nrows, dm, dv, c->stream);
+    // scratch is released on every path (stream-ordered)
+    struct Scratch {
+        cudaStream_t s;
+        void *p[3];
+        ~Scratch() {
+            for (void *q : p)
+                if (q) cudaFreeAsync(q, s);
+        }
+    } guard{s, {nullptr, nullptr, nullptr}};
+    CUDA_TRY(cudaMallocAsync(&dX, (size_t)nrows * f->nfeat * sizeof(double), s));
+    guard.p[0] = dX;
+    CUDA_TRY(cudaMallocAsync(&dm, (size_t)nrows * sizeof(double), s));
+    guard.p[1] = dm;
+    if (h_votes) {
+        CUDA_TRY(cudaMallocAsync(&dv, (size_t)nrows * sizeof(int32_t), s));
+        guard.p[2] = dv;
+    }
+    CUDA_TRY(cudaMemcpyAsync(dX, h_X, (size_t)nrows * f->nfeat * sizeof(double), cudaMemcpyHostToDevice, s));
+    int rc = lmt_rf_mean(f, dX, nrows, dm, dv, s);
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(h_mean, dm, (size_t)nrows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (h_votes) CUDA_TRY(cudaMemcpyAsync(h_votes, dv, (size_t)nrows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaFreeAsync(dX, c->stream));
-    CUDA_TRY(cudaFreeAsync(dm, c->stream));
-    if (dv) CUDA_TRY(cudaFreeAsync(dv, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpyAsync(h_mean, dm, (size_t)nrows * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (h_votes) CUDA_TRY(cudaMemcpyAsync(h_votes, dv, (size_t)nrows * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return LMT_OK;
 }
 

@@ -1,28 +1,14 @@
-// lmt_kernels.cuh -- sm_100a device code of the lmtune hot path.
+// lmt_kernels.cuh -- ahead-of-time sm_100a device code of the lmtune hot path
+// (the synthetic kernel itself, K1/K2, is specialised per instance at run
+// time: lmt_jit.cuh).
 //
 //   K0 k_fill          interp._hash_fill / make_inputs   (interp.py:22-38)
-//   K1 k_synth_base    baseline variant: plain global loads
-//                      (codegen.py:240-333 BASELINE, executed by interp.py:83-113)
-//   K2 k_synth_opt     local-memory variant: the workgroup's region is staged
-//                      into shared memory by TMA (cp.async.bulk.tensor) behind
-//                      mbarriers, double/multi-buffered across work-unit
-//                      iterations (codegen.py:273-312, interp.py:71-98)
+//      k_in2_halo, k_in2_shift, k_in_shift   input layouts K1/K2 read
 //   K2b k_digest       order-independent output digest + base/opt comparison
+//      k_gather        sampled output cells (the oracle spot check)
+//      k_scrub         L2 flush between timed variants
 //   K3 k_rf_mean       random-forest mean, warp per sample, lane per tree,
 //                      ballot vote (forest.py:49-58, 208-218)
-//
-// Numerics (bit-exact with the numpy interpreter):
-//   * every `acc += x` is a single-rounded fp32 add (__fadd_rn), in the
-//     reference order: stencil offsets row-major (kernel_model.py:122-130),
-//     comp_ilb MADs, coal_ilb reads, uncoal_ilb reads, then the epilogue.
-//   * MAD: numpy computes RN(RN(acc*c1) + c2) (interp.py:101) with
-//     c1 in {2, 0.5} and |c2| >= 1/64 (codegen.py:58-66). acc*c1 is exact
-//     except (a) overflow, where acc*2 >= 2^128 so both forms give inf, and
-//     (b) |acc| < 2^-125 with c1 = 0.5, where the lost bits are < 2^-150 and
-//     cannot move RN(c2 + tiny) off c2. Hence RN(acc*c1 + c2) (one FFMA) is
-//     bit-identical; tests/test_gpu_parity.py checks it on +-inf-producing
-//     instances too.
-//   * no fast-math, no FTZ (nvcc default), so subnormals are preserved.
 #pragma once
 
 #include <cuda.h>
@@ -32,304 +18,6 @@
 #include "lmt_args.h"
 
 namespace lmt {
-
-constexpr int kMaxStages = 4;
-
-// ---------------------------------------------------------------- helpers
-
-__device__ __forceinline__ constexpr bool in_stencil(int shape, int r, int dr, int dc) {
-    // kernel_model.py:123-129; shape 0 rect, 1 diamond, 2 star
-    return shape == 0 ? true
-         : shape == 1 ? ((dr < 0 ? -dr : dr) + (dc < 0 ? -dc : dc) <= r)
-                      : (dr == 0 || dc == 0);
-}
-
-__device__ __forceinline__ float ldg_f(const float *p) {
-    float v;
-    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-
-// k-th MAD constants, phase p = k % 10 (codegen.py:58-66): c1 alternates
-// 2 / 0.5 on k % 2, c2 = +-(1 + k % 5) / 64 with the sign of k % 2.
-__device__ __forceinline__ constexpr float mad_c1(int p) { return (p & 1) ? 0.5f : 2.0f; }
-__device__ __forceinline__ constexpr float mad_c2(int p) {
-    return ((p & 1) ? -1.0f : 1.0f) * (float)(1 + p % 5) * (1.0f / 64.0f);
-}
-
-// The in-loop MAD chain: k = 0 .. comp_ilb-1 restarts every (i, j)
-// (codegen.py:217-219), so it is 10-blocks of immediates plus a tail.
-__device__ __forceinline__ float mad_ilb(float acc, int q, int rem) {
-    for (int u = 0; u < q; ++u) {
-#pragma unroll
-        for (int p = 0; p < 10; ++p) acc = __fmaf_rn(acc, mad_c1(p), mad_c2(p));
-    }
-#pragma unroll
-    for (int p = 0; p < 9; ++p)
-        if (p < rem) acc = __fmaf_rn(acc, mad_c1(p), mad_c2(p));
-    return acc;
-}
-
-// Epilogue chain: k = comp_ilb + 0 .. comp_ep-1 (codegen.py:229-231).
-__device__ __forceinline__ float mad_ep(float acc, int count, int phase) {
-    for (int k = 0; k < count; ++k) {
-        const int p = phase;
-        const float c1 = (p & 1) ? 0.5f : 2.0f;
-        const float c2 = ((p & 1) ? -1.0f : 1.0f) * (float)(1 + p % 5) * (1.0f / 64.0f);
-        acc = __fmaf_rn(acc, c1, c2);
-        phase = (phase == 9) ? 0 : phase + 1;
-    }
-    return acc;
-}
-
-__device__ __forceinline__ int wrap_add(int base, int k, int mod) {
-    // (base + k) % mod for 0 <= base < mod, k >= 0
-    int r = base + k;
-    if (r >= mod) r = (r - mod < mod) ? r - mod : r % mod;
-    return r;
-}
-
-// Contextual in2 reads (codegen.py:220-223, 232-235):
-//   coal:   in2[(t + k) % IN2_H][glin % IN2_W]
-//   uncoal: in2[glin % IN2_H][(t + k) % IN2_W]
-// in2c points at column glin % IN2_W, in2u at row glin % IN2_H.
-__device__ __forceinline__ float ctx_reads(float acc, const float *in2c, const float *in2u,
-                                           int trow, int tcol, int ncoal, int nuncoal,
-                                           int H2, int W2, int P2) {
-    for (int k = 0; k < ncoal; ++k) acc = __fadd_rn(acc, ldg_f(in2c + (size_t)wrap_add(trow, k, H2) * P2));
-    for (int k = 0; k < nuncoal; ++k) acc = __fadd_rn(acc, ldg_f(in2u + wrap_add(tcol, k, W2)));
-    return acc;
-}
-
-// ------------------------------------------------------- target-array sources
-
-// Baseline: every target access is a global load (read-only path, L1/L2).
-struct GlobalSrc {
-    const float *base;  // element (home row 0, home col 0) incl. PAD
-    int P;
-    __device__ __forceinline__ const float *at(int hr, int hc) const { return base + (hr * P + hc); }
-    __device__ __forceinline__ float load(const float *p, int dr, int dc) const { return ldg_f(p + dr * P + dc); }
-};
-
-// Optimized, single column chunk: region row-major with pitch bw.
-struct SmemSrc {
-    const float *base;  // region element (0,0) for this thread's work unit origin
-    int bw;
-    __device__ __forceinline__ const float *at(int hr, int hc) const { return base + (hr * bw + hc); }
-    __device__ __forceinline__ float load(const float *p, int dr, int dc) const { return p[dr * bw + dc]; }
-};
-
-// Optimized, several 256-wide column chunks: [ccol][rows][256].
-struct SmemWideSrc {
-    const float *slot;
-    int chunk;  // rows_padded * 256
-    int hr, hc;
-    __device__ __forceinline__ SmemWideSrc at(int r, int c) const { return SmemWideSrc{slot, chunk, r, c}; }
-    __device__ __forceinline__ float load(const SmemWideSrc &s, int dr, int dc) const {
-        const int c = s.hc + dc;
-        return s.slot[(c >> 8) * chunk + (s.hr + dr) * 256 + (c & 255)];
-    }
-};
-
-template <int SHAPE, int R, class Src, class Ptr>
-__device__ __forceinline__ float stencil_sum(float acc, const Src &src, const Ptr &p,
-                                             const SynthArgs &A) {
-    if constexpr (R >= 0) {
-#pragma unroll
-        for (int dr = -R; dr <= R; ++dr) {
-#pragma unroll
-            for (int dc = -R; dc <= R; ++dc) {
-                if (in_stencil(SHAPE, R, dr, dc)) acc = __fadd_rn(acc, src.load(p, dr, dc));
-            }
-        }
-    } else {
-        for (int k = 0; k < A.K; ++k) acc = __fadd_rn(acc, src.load(p, A.sdr[k], A.sdc[k]));
-    }
-    return acc;
-}
-
-// One work unit, i/j loop nest + epilogue (codegen.py:314-323 and the
-// bodies _inner_body 207-224, _epilogue 227-237). (hr0, hc0) is the home
-// coordinate of (i=0, j=0) in the source's coordinate frame.
-template <int SHAPE, int R, class Src>
-__device__ __forceinline__ float work_unit(const SynthArgs &A, const Src &src, int hr0, int hc0,
-                                           const float *in2c, const float *in2u) {
-    float acc = 0.0f;
-    int trow = 0, tcol = 0;  // (i*M + j) % IN2_H, % IN2_W
-    for (int i = 0; i < A.N; ++i) {
-        int hr = hr0 + A.a[2] * i;
-        int hc = hc0 + A.a[6] * i;
-        for (int j = 0; j < A.M; ++j) {
-            const auto p = src.at(hr, hc);
-            acc = stencil_sum<SHAPE, R>(acc, src, p, A);
-            acc = mad_ilb(acc, A.comp_q, A.comp_rem);
-            acc = ctx_reads(acc, in2c, in2u, trow, tcol, A.coal_ilb, A.uncoal_ilb, A.H2, A.W2, A.P2);
-            hr += A.a[3];
-            hc += A.a[7];
-            trow = (trow + 1 == A.H2) ? 0 : trow + 1;
-            tcol = (tcol + 1 == A.W2) ? 0 : tcol + 1;
-        }
-    }
-    acc = mad_ep(acc, A.comp_ep, A.comp_ep_phase);
-    acc = ctx_reads(acc, in2c, in2u, A.ep_row0, A.ep_col0, A.coal_ep, A.uncoal_ep, A.H2, A.W2, A.P2);
-    return acc;
-}
-
-// ------------------------------------------------------------------- K1
-
-// blockDim = (WG_W, WG_H), gridDim = (GRID_X/WG_W, GRID_Y/WG_H): one CTA per
-// workgroup, one thread per workitem, work units blocked across workgroups
-// and cyclic across workitems (kernel_model.py:158-170).
-template <int SHAPE, int R>
-__global__ void __launch_bounds__(1024, 1) k_synth_base(const SynthArgs A) {
-    const int wi_x = threadIdx.x, wi_y = threadIdx.y;
-    const int wg_w = blockDim.x, wg_h = blockDim.y;
-    const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
-    const float *in2c = A.in2 + (glin % A.W2);
-    const float *in2u = A.in2 + (size_t)(glin % A.H2) * A.P2;
-    const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
-    const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
-    const GlobalSrc src{A.in + (A.pad * A.P + A.pad), A.P};
-    for (int iy = 0; iy < A.nwy; ++iy) {
-        const int wu_y = wuy0 + iy * wg_h;
-        for (int ix = 0; ix < A.nwx; ++ix) {
-            const int wu_x = wux0 + ix * wg_w;
-            const int hr0 = A.a[0] * wu_x + A.a[1] * wu_y;
-            const int hc0 = A.a[4] * wu_x + A.a[5] * wu_y;
-            const float acc = work_unit<SHAPE, R>(A, src, hr0, hc0, in2c, in2u);
-            A.out[(size_t)wu_y * A.out_w + wu_x] = acc;
-        }
-    }
-}
-
-// ------------------------------------------------------------------- K2
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE;\n\t"
-        "bra LAB_WAIT;\n"
-        "DONE:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(float *dst, const CUtensorMap *map, uint64_t *bar, int x, int y) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-        : "memory");
-}
-
-// Stage the region of work-unit iteration `it` into slot `slot`
-// (the cooperative copy of codegen.py:296-311, done by the TMA engine).
-__device__ __forceinline__ void stage_region(const SynthArgs &A, const CUtensorMap *map, float *smem,
-                                             uint64_t *full, int slot, int it) {
-    const int ix = it % A.nwx, iy = it / A.nwx;
-    const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
-    const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
-    // region origin (codegen.py:291-295) shifted into the PAD-ed `in` frame.
-    // The innermost TMA box coordinate must be 16-byte aligned (measured on
-    // B200: an unaligned x raises an illegal-instruction fault), so the box
-    // starts at org_col rounded down to 4 floats and the region sits at
-    // column (org_col & 3) of the staged rows (see region_shift()).
-    const int org_row = A.a[0] * wu_x0 + A.a[1] * wu_y0 + A.off_min_row + A.pad;
-    const int org_col = (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & ~3;
-    float *dst = smem + slot * A.stage_floats;
-    mbar_expect_tx(&full[slot], A.stage_bytes);
-    for (int cc = 0; cc < A.ncc; ++cc)
-        for (int rc = 0; rc < A.nrc; ++rc)
-            tma_load_2d(dst + (cc * A.nrc + rc) * A.bh * A.bw, map, &full[slot], org_col + cc * A.bw,
-                        org_row + rc * A.bh);
-}
-
-// Column of the staged rows where region column 0 landed for iteration it.
-__device__ __forceinline__ int region_shift(const SynthArgs &A, int it) {
-    const int ix = it % A.nwx, iy = it / A.nwx;
-    const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
-    const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
-    return (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & 3;
-}
-
-template <int SHAPE, int R, bool WIDE>
-__global__ void __launch_bounds__(1024, 1)
-    k_synth_opt(const __grid_constant__ CUtensorMap tmap, const SynthArgs A) {
-    extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
-
-    const int wi_x = threadIdx.x, wi_y = threadIdx.y;
-    const int wg_w = blockDim.x, wg_h = blockDim.y;
-    const int tid = wi_y * wg_w + wi_x;
-    const int nthreads = wg_w * wg_h;
-    const int nwarps = (nthreads + 31) >> 5;
-    const int lane = tid & 31;
-    const int S = A.nstages;
-    const int nit = A.nwx * A.nwy;
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], nwarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-        for (int s = 0; s < S && s < nit; ++s) stage_region(A, &tmap, smem, full, s, s);
-    }
-
-    const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
-    const float *in2c = A.in2 + (glin % A.W2);
-    const float *in2u = A.in2 + (size_t)(glin % A.H2) * A.P2;
-    // home coordinate of (i=0, j=0) relative to the region origin is the same
-    // for every iteration: (a0*wi_x + a1*wi_y - off_min_row, ...)
-    const int hr0 = A.a[0] * wi_x + A.a[1] * wi_y - A.off_min_row;
-    const int hc0 = A.a[4] * wi_x + A.a[5] * wi_y - A.off_min_col;
-    const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
-    const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
-
-    for (int it = 0; it < nit; ++it) {
-        const int slot = it % S;
-        // refill the slot of the previous iteration once every warp released it
-        if (tid == 0 && it > 0 && it - 1 + S < nit) {
-            const int ps = (it - 1) % S;
-            mbar_wait(&empty[ps], ((it - 1) / S) & 1);
-            stage_region(A, &tmap, smem, full, ps, it - 1 + S);
-        }
-        mbar_wait(&full[slot], (it / S) & 1);
-        const float *region = smem + slot * A.stage_floats;
-        const int sh = region_shift(A, it);
-        float acc;
-        if constexpr (WIDE) {
-            const SmemWideSrc src{region, A.nrc * A.bh * 256, 0, 0};
-            acc = work_unit<SHAPE, R>(A, src, hr0, hc0 + sh, in2c, in2u);
-        } else {
-            const SmemSrc src{region + sh, A.bw};
-            acc = work_unit<SHAPE, R>(A, src, hr0, hc0, in2c, in2u);
-        }
-        const int ix = it % A.nwx, iy = it / A.nwx;
-        A.out[(size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w)] = acc;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-}
 
 // ------------------------------------------------------------------- K0
 
@@ -397,6 +85,21 @@ __global__ void k_in_shift(float *__restrict__ buf, long long rows, long long P)
     }
 }
 
+// The four shifted copies of a shared `in` ([rows][P]) in a lane's own
+// buffer: dst[s * rows * P + r * P + x] = src[r * P + x + s] (0 past the
+// row), s = 0..3 -- the baseline's 128-bit row layout, built inside its
+// timed window.
+__global__ void k_in_copy4(const float *__restrict__ src, float *__restrict__ dst, long long rows, long long P) {
+    const long long n = rows * P;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n * kInCopies;
+         v += (long long)gridDim.x * blockDim.x) {
+        const long long cs = v / n, rem = v - cs * n;
+        const long long r = rem / P, x = rem - r * P;
+        const int s = (int)cs;
+        dst[v] = (x + s < P) ? src[r * P + x + s] : 0.0f;
+    }
+}
+
 // ---------------------------------------------------------------- digest
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -449,6 +152,40 @@ __global__ void k_digest(const float *__restrict__ a, const float *__restrict__ 
             }
         }
     }
+}
+
+// -------------------------------------------------------- measurement aids
+
+// Sampled output cells of both variants: vals[2k] = a[idx[k]], vals[2k+1] =
+// b[idx[k]] (b may be null). The caller checks them against the CPU oracle.
+__global__ void k_gather(const float *__restrict__ a, const float *__restrict__ b, const int64_t *__restrict__ idx,
+                         int n, float *__restrict__ vals) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int64_t i = idx[k];
+        vals[2 * k] = a[i];
+        vals[2 * k + 1] = b ? b[i] : 0.0f;
+    }
+}
+
+// L2 flush: stream `n4` float4 stores through a buffer larger than the
+// 126 MB L2 (write-allocate evicts every line the timed kernel could hit).
+// `tag` changes per call so the stores are never redundant.
+__global__ void k_scrub(float4 *__restrict__ buf, int64_t n4, float tag) {
+    const float4 v = make_float4(tag, tag, tag, tag);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = v;
+}
+
+// A head start for an idle stream: one thread spins for `ns` nanoseconds
+// so that the host has enqueued the event and the kernel behind it before
+// the GPU reaches them (an event recorded on an idle stream would otherwise
+// time the host's launch latency too).
+__global__ void k_lead(long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < (unsigned long long)ns);
 }
 
 // ------------------------------------------------------------------- K3

@@ -22,7 +22,11 @@ from ._lib import (
     LMT_ERR_INFEASIBLE,
     LMT_OK,
     MEASURE_ALLOW_LARGE_LMEM,
+    MEASURE_CONCURRENT,
+    MEASURE_REGBLOCK,
     MEASURE_SKIP_OPT,
+    MEASURE_WARM_L2,
+    CMeasureOpts,
     CMeasurement,
     check,
     last_error,
@@ -51,6 +55,10 @@ class Measurement:
     kernel_id: int
     launches: int
     nstages: int
+    lane_sms: int = 0               # SM partition it ran in (0 = the whole device, L2 flushed per variant)
+    order: int = 0                  # 1: the optimized variant was timed first
+    in_copies: int = 1              # 4: the baseline built and read 128-bit shifted copies (inside t_base)
+    ctas: int = 0
 
     @property
     def ok(self) -> bool:
@@ -83,15 +91,25 @@ def _convert(instances, raw) -> list[Measurement]:
             digest_base=int(m.digest_base), digest_opt=int(m.digest_opt) if ran_opt else None,
             mismatches=int(m.mismatches), alg_bytes=m.alg_bytes, alg_flops=m.alg_flops,
             t_fill_ms=m.t_fill_ms, status=int(m.status), kernel_id=int(m.kernel_id),
-            launches=int(m.launches), nstages=int(m.nstages),
+            launches=int(m.launches), nstages=int(m.nstages), lane_sms=int(m.lane_sms), order=int(m.order),
+            in_copies=int(m.in_copies), ctas=int(m.ctas),
         ))
     return out
 
 
-def measure_raw(instances, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False,
-                chunk: int = 4096):
+def measure_flags(*, skip_opt: bool = False, allow_large_lmem: bool = False, concurrent: bool = False,
+                  regblock: bool = False, warm_l2: bool = False) -> int:
+    """lmt_measure_batch flags (include/lmt_b200.h). Defaults are the
+    measurement contract: every instance on the whole device, L2 flushed
+    before each variant, each work unit issuing its own loads."""
+    return ((MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+            | (MEASURE_CONCURRENT if concurrent else 0) | (MEASURE_REGBLOCK if regblock else 0)
+            | (MEASURE_WARM_L2 if warm_l2 else 0))
+
+
+def measure_raw(instances, dev=DEFAULT_DEVICE, *, chunk: int = 4096, **kw):
     """lmt_measure_batch over ``instances``; returns the raw ctypes records."""
-    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    flags = measure_flags(**kw)
     cdev = c_device(dev)
     res = []
     for s in range(0, len(instances), chunk):
@@ -103,28 +121,39 @@ def measure_raw(instances, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_
     return res
 
 
-def measure_records(records, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False):
+def measure_records(records, dev=DEFAULT_DEVICE, *, samples: np.ndarray | None = None, **kw):
     """Measure an int32 [n, 19] record table (sweep.InstanceTable.records);
-    returns a numpy structured view of the lmt_measurement records."""
+    returns a numpy structured view of the lmt_measurement records. With
+    ``samples`` (int64 [n, S] linear output indices) returns
+    ``(records, values)``, values float32 [n, S, 2] = the baseline and
+    optimized output at those cells, for an independent (oracle) check."""
     from .sweep import records_to_c
 
-    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
     n = len(records)
     arr = records_to_c(records)
     out = (CMeasurement * max(n, 1))()
-    check(lib().lmt_measure_batch(arr, n, ctypes.byref(c_device(dev)), flags, out), what="measure_batch")
-    return np.frombuffer(out, dtype=MEASUREMENT_DTYPE, count=n).copy()
+    opts = CMeasureOpts(measure_flags(**kw), 0, None, None)
+    vals = None
+    if samples is not None:
+        samples = np.ascontiguousarray(samples, dtype=np.int64).reshape(n, -1)
+        vals = np.zeros((n, samples.shape[1], 2), dtype=np.float32)
+        opts.samples = samples.shape[1]
+        opts.sample_idx = samples.ctypes.data
+        opts.h_sample_vals = vals.ctypes.data
+    check(lib().lmt_measure_batch_ex(arr, n, ctypes.byref(c_device(dev)), ctypes.byref(opts), None, None, None,
+                                     None, None, None, out), what="measure_batch")
+    res = np.frombuffer(out, dtype=MEASUREMENT_DTYPE, count=n).copy()
+    return res if samples is None else (res, vals)
 
 
-def prepare_records(records, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False,
-                    nthreads: int = 0) -> int:
+def prepare_records(records, dev=DEFAULT_DEVICE, *, nthreads: int = 0, **kw) -> int:
     """Compile (NVRTC, sm_100a) and load every specialised kernel that
     measuring ``records`` will launch -- the reference's per-kernel compile
     step (codegen.py:150-182) -- in parallel host threads. Returns the number
     of distinct kernels the batch needs."""
     from .sweep import records_to_c
 
-    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    flags = measure_flags(**kw)
     n = len(records)
     arr = records_to_c(records)
     out = ctypes.c_int64()
@@ -133,10 +162,9 @@ def prepare_records(records, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allo
     return int(out.value)
 
 
-def prepare_instances(instances, dev=DEFAULT_DEVICE, *, skip_opt: bool = False, allow_large_lmem: bool = False,
-                      nthreads: int = 0) -> int:
+def prepare_instances(instances, dev=DEFAULT_DEVICE, *, nthreads: int = 0, **kw) -> int:
     """prepare_records for KernelInstance objects."""
-    flags = (MEASURE_SKIP_OPT if skip_opt else 0) | (MEASURE_ALLOW_LARGE_LMEM if allow_large_lmem else 0)
+    flags = measure_flags(**kw)
     instances = list(instances)
     out = ctypes.c_int64()
     check(lib().lmt_prepare(to_c_array(instances), len(instances), ctypes.byref(c_device(dev)), flags, nthreads,
@@ -148,6 +176,7 @@ MEASUREMENT_DTYPE = np.dtype([
     ("t_base_ms", "f8"), ("t_opt_ms", "f8"), ("digest_base", "u8"), ("digest_opt", "u8"),
     ("mismatches", "i8"), ("alg_bytes", "f8"), ("alg_flops", "f8"), ("t_fill_ms", "f8"),
     ("status", "i4"), ("kernel_id", "i4"), ("launches", "i4"), ("nstages", "i4"),
+    ("lane_sms", "i4"), ("order", "i4"), ("in_copies", "i4"), ("ctas", "i4"),
 ])
 
 
@@ -157,7 +186,7 @@ def measure_instances(instances, dev=DEFAULT_DEVICE, **kw) -> list[Measurement]:
 
 
 def measure_instances_host(instances, in_arrays, in2_arrays, dev=DEFAULT_DEVICE, *, out_base=None,
-                           out_opt=None, skip_opt: bool = False) -> list[Measurement]:
+                           out_opt=None, samples: np.ndarray | None = None, **kw):
     """End-to-end variant: instance i's inputs come from host arrays (ideally
     pinned) and are copied to the device inside the timed batch; outputs are
     optionally copied back into ``out_base[i]`` / ``out_opt[i]``."""
@@ -185,11 +214,19 @@ def measure_instances_host(instances, in_arrays, in2_arrays, dev=DEFAULT_DEVICE,
     cols = (ctypes.c_int64 * max(n, 1))(*[int(x.shape[1]) for x in in_arrays])
     arr = to_c_array(instances)
     out = (CMeasurement * max(n, 1))()
-    flags = MEASURE_SKIP_OPT if skip_opt else 0
-    rc = lib().lmt_measure_batch_host(arr, n, ctypes.byref(c_device(dev)), flags, ptrs(in_arrays), rows, cols,
-                                      ptrs(in2_arrays), ptrs(out_base, True), ptrs(out_opt, True), out)
+    opts = CMeasureOpts(measure_flags(**kw), 0, None, None)
+    vals = None
+    if samples is not None:
+        samples = np.ascontiguousarray(samples, dtype=np.int64).reshape(n, -1)
+        vals = np.zeros((n, samples.shape[1], 2), dtype=np.float32)
+        opts.samples = samples.shape[1]
+        opts.sample_idx = samples.ctypes.data
+        opts.h_sample_vals = vals.ctypes.data
+    rc = lib().lmt_measure_batch_ex(arr, n, ctypes.byref(c_device(dev)), ctypes.byref(opts), ptrs(in_arrays), rows,
+                                    cols, ptrs(in2_arrays), ptrs(out_base, True), ptrs(out_opt, True), out)
     check(rc, what="measure_batch_host")
-    return _convert(instances, out[:n])
+    ms = _convert(instances, out[:n])
+    return ms if samples is None else (ms, vals)
 
 
 def launch_floor(records: np.ndarray, res: np.ndarray, hbm_gbs: float) -> dict:

@@ -92,16 +92,19 @@ def test_emit_optimized_infeasible(golden):
 
 def test_shared_load_paths_are_exercised_by_the_goldens(golden):
     """LMT_SHARE (one load per tap for a group of work units with the same
-    home coordinate) is only ever enabled for xy_reuse / x_reuse_* and the
-    golden parity set (run bitwise on the GPU) reaches it for both kinds,
-    in both variants."""
+    home coordinate) is off in the literal kernels (the measurement
+    contract), only ever enabled for xy_reuse / x_reuse_* in the register-
+    blocked ones, and the golden parity set (run bitwise on the GPU in both
+    modes) reaches it for both kinds, in both variants."""
     seen = {}
     for r in golden["interp"]:
         inst = make_instance(r)
-        for variant, src in (("base", L.emit_baseline(inst)), ("opt", None)):
+        assert dict(L.emit_baseline(inst).compile_defines)["LMT_SHARE"] == 0
+        for variant, src in (("base", L.emit_baseline(inst, regblock=True)), ("opt", None)):
             if variant == "opt":
                 try:
-                    src = L.emit_optimized(inst)
+                    src = L.emit_optimized(inst, regblock=True)
+                    assert dict(L.emit_optimized(inst).compile_defines)["LMT_SHARE"] == 0
                 except L.OptimizationInfeasible:
                     continue
             d = dict(src.compile_defines)

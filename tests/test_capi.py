@@ -54,7 +54,8 @@ def test_struct_layouts_match_header():
 
     assert ctypes.sizeof(_lib.CInstance) == 19 * 4
     assert ctypes.sizeof(_lib.CDevice) == 10 * 4
-    assert ctypes.sizeof(_lib.CMeasurement) == 8 * 8 + 4 * 4
+    assert ctypes.sizeof(_lib.CMeasurement) == 8 * 8 + 8 * 4
+    assert ctypes.sizeof(_lib.CMeasureOpts) == 4 + 4 + 8 + 8
 
 
 def test_missing_library_fails_loudly(monkeypatch, tmp_path):

@@ -346,3 +346,71 @@ def test_edge_paths_against_oracle():
         assert np.array_equal(opt_out, want_b), inst
         m = L.measure_instances([inst])[0]
         assert m.verified and m.digest_base == oracle.out_hash(want_b)
+
+
+def test_measure_modes_bitwise(golden):
+    """The measurement modes (SM partitions, register-blocked variants, warm
+    L2) change where and how the kernels run, never their outputs: every
+    golden instance's digests match the reference's in every mode, and the
+    few-CTA instances really ran inside partitions."""
+    recs = golden["interp"][::2]
+    cases = [make_instance(r) for r in recs]
+    for kw in (dict(concurrent=True), dict(regblock=True), dict(concurrent=True, regblock=True, warm_l2=True)):
+        L.prepare_instances(cases, **kw)
+        ms = L.measure_instances(cases, **kw)
+        for m, r in zip(ms, recs):
+            assert m.status == 0, (kw, m.status, L.measure.last_error())
+            assert m.verified and m.digest_base == int(r["digest"]) == m.digest_opt, (kw, r)
+        if kw.get("concurrent") and L._lib.partitions():
+            biggest = max(L._lib.partitions())
+            assert all((m.lane_sms > 0) == (m.ctas <= biggest) for m in ms)
+            assert all(m.lane_sms >= m.ctas for m in ms if m.lane_sms > 0)
+            assert any(m.lane_sms > 0 for m in ms)
+
+
+def test_sampled_cells_match_oracle_at_full_size():
+    """Paper-geometry instances of the 1M sweep (2048^2 outputs, `in` up to
+    ~1 GiB), both variants, measured in SM partitions: the cells gathered by
+    the measurement equal the CPU oracle's point evaluation of
+    interp.execute bit for bit -- an independent check of K1 and K2 (not
+    just K1 == K2)."""
+    sys_path_bench()
+    import bench
+
+    tab = L.select_instance_table(L.SamplingSpec(max_instances=1_000_000, seed=0))
+    rng = np.random.default_rng(11)
+    rows = np.sort(rng.choice(len(tab), size=400, replace=False))
+    rec = tab.records(rows)
+    keep = L.sweep.launch_cost(rec) < 0.4
+    rec = rec[keep][:48]
+    idx = bench.sample_cells(rec, 24, 3)
+    L.prepare_records(rec, concurrent=True)
+    res, vals = L.measure_records(rec, samples=idx, concurrent=True)
+    assert (res["status"] != 1).all() and (res["t_base_ms"] > 0).all()
+    orc = bench.oracle_check(rec, res, idx, vals)
+    assert orc["instances"] == len(rec) and orc["mismatched"] == 0, orc
+    assert (res["mismatches"][res["t_opt_ms"] > 0] == 0).all()
+
+
+def test_vec_baseline_charges_its_layout():
+    """A radius-2 instance whose baseline reads 128-bit shifted copies of
+    `in`: the copy is built inside the baseline's timed window
+    (in_copies == 4) and the output is still the reference's."""
+    P, S = L.HomeAccessPattern, L.StencilShape
+    params = L.TemplateParams(2048, 2048, 2048, 2048, P.Y_REUSE_ROW, 32, 8, L.StencilPattern(S.RECTANGULAR, 2),
+                              num_comp_ilb=10, num_comp_ep=3, num_coal_ilb=2, num_coal_ep=1, num_uncoal_ilb=1,
+                              num_uncoal_ep=2)
+    inst = L.KernelInstance(params, L.LaunchConfig(128, 16, 32, 8))
+    rec = L.sweep.instances_to_records([inst])
+    idx = np.array([[0, 1, 2047, 2048 * 2048 - 1, 12345, 777777]], dtype=np.int64)
+    res, vals = L.measure_records(rec, samples=idx)
+    assert res["in_copies"][0] == 4 and res["mismatches"][0] == 0
+    for v in (0, 1):
+        assert np.array_equal(vals[0, :, v].view(np.uint32), oracle.eval_units(rec[0], v, idx[0]).view(np.uint32))
+
+
+def sys_path_bench():
+    import sys
+
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
