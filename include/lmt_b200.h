@@ -275,6 +275,11 @@ int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int varia
  * compiles) and the host seconds spent compiling. */
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);
 
+/* The current CUDA device of the calling thread (the device every other
+ * entry point works on; a forest handle is bound to the device it was
+ * created on and lmt_rf_mean rejects it on another). */
+int lmt_current_device(int32_t *dev_out);
+
 /* Synchronise the library stream of the current device. */
 int lmt_sync(void);
 

@@ -1884,6 +1884,14 @@ int lmt_get_stream(void **stream_out) {
     return LMT_OK;
 }
 
+int lmt_current_device(int32_t *dev_out) {
+    if (!dev_out) return fail(LMT_ERR_ARG, "null argument");
+    int d = 0;
+    CUDA_TRY(cudaGetDevice(&d));
+    *dev_out = d;
+    return LMT_OK;
+}
+
 int lmt_sync(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     DevCtx *c;
@@ -1982,6 +1990,8 @@ int lmt_rf_mean(const lmt_forest *f, const double *d_X, int64_t nrows, double *d
         int rc = get_ctx(&c);
         if (rc) return rc;
     }
+    if (c->device != f->device)
+        return fail(LMT_ERR_ARG, "forest was uploaded to device %d, current device is %d", f->device, c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t warps = (nrows + 0);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)c->sms * 8));

@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes
 import math
 import threading
+import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -213,16 +214,31 @@ class GpuForest:
 
 
 _cache_lock = threading.Lock()
-_cache: dict[int, tuple[object, tuple, GpuForest]] = {}
+_cache: dict[tuple, tuple[object, tuple, GpuForest]] = {}
 
 
 def _fingerprint(forest) -> tuple:
-    return tuple((id(t.feature), len(t.feature), id(t.threshold), id(t.value)) for t in forest.trees)
+    """Content of every tree (crc32 of its arrays, cheap next to a predict),
+    so trees edited in place are re-uploaded like the reference re-reads them."""
+    fp = []
+    for t in forest.trees:
+        h = 0
+        for a in (t.feature, t.threshold, t.left, t.right, t.value):
+            h = zlib.crc32(np.ascontiguousarray(a).tobytes(), h)
+        fp.append((len(t.feature), h))
+    return tuple(fp)
+
+
+def _current_device() -> int:
+    d = ctypes.c_int32(0)
+    check(lib().lmt_current_device(ctypes.byref(d)), what="current_device")
+    return int(d.value)
 
 
 def gpu_forest(forest) -> GpuForest:
-    """Upload once per forest object (cached while its trees are unchanged)."""
-    key = id(forest)
+    """Upload once per (forest object, CUDA device), re-uploaded when the
+    trees' contents change."""
+    key = (id(forest), _current_device())
     fp = _fingerprint(forest)
     with _cache_lock:
         hit = _cache.get(key)
