@@ -123,6 +123,11 @@ typedef struct lmt_measure_opts {
     int32_t samples;            /* output cells gathered per instance (0: none) */
     const int64_t *sample_idx;  /* [n][samples] linear indices into out (row * out_w + col) */
     float *h_sample_vals;       /* [n][samples][2]: baseline, optimized value (0 when not run) */
+    /* Kernel-shape overrides for tuning studies, 0 = the library's choice:
+     * baseline work units per thread, prefetch depth, min resident CTAs per
+     * SM; optimized work units per thread, staging slots, min resident CTAs.
+     * Outputs do not depend on them (every shape is bit-identical). */
+    int32_t tune[6];
 } lmt_measure_opts;
 
 const char *lmt_version(void);

@@ -86,6 +86,7 @@ class CMeasureOpts(ctypes.Structure):
     _fields_ = [
         ("flags", ctypes.c_int32), ("samples", ctypes.c_int32),
         ("sample_idx", ctypes.c_void_p), ("h_sample_vals", ctypes.c_void_p),
+        ("tune", ctypes.c_int32 * 6),
     ]
 
 

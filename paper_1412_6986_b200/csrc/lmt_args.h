@@ -33,6 +33,9 @@ struct SynthArgs {
     // floats between the kInCopies shifted copies of `in` (0: one copy only);
     // copy_s[r][x] = in[r][x + s] (see k_in_shift)
     long long in_copy;
+    // log2(nwx) when the number of work-unit columns per workitem is a power
+    // of two (iteration -> (ix, iy) by shift and mask), else -1 (division)
+    int nwx_shift;
 };
 
 // Shifted copies of `in` for the baseline's 128-bit loads of stencil rows

@@ -543,12 +543,66 @@ bool jit_share(const SynthArgs &A, int U, bool regblock) {
 }
 
 void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, int64_t ctas, int64_t warps,
-                int64_t nit, int64_t sms, bool opt, int64_t stage_bytes, int64_t smem_cap, bool regblock, int *U_out,
-                int *D_out, int *S_out) {
+                int64_t nit, int64_t sms, bool opt, int64_t stage_bytes, int64_t smem_cap, bool regblock, bool membound,
+                int *U_out, int *D_out, int *S_out, int *minb_out) {
     auto sets = [&](int U) -> int64_t { return jit_share(A, U, regblock) ? 1 : U; };
-    int bu = 1, bd = 3, bs = 1;
+    const int64_t nm = (int64_t)p.n * p.m;  // (i, j) steps per work unit: a deeper prefetch ring is dead weight
+    const int dmax = (int)std::min<int64_t>(3, std::max<int64_t>(1, nm));
+    int bu = 1, bd = dmax, bs = 1;
+    if (minb_out) *minb_out = 1;
     for (int U : {16, 8, 4, 2, 1})
         if (U <= nit) { bu = U; break; }
+    // optimized variant: U work units per thread and a ring of G group
+    // stages, each holding the regions of one group of U iterations (one
+    // region when the group's units share it) behind one mbarrier pair.
+    auto rps = [&](int U) -> int64_t { return jit_share(A, U, regblock) ? 1 : U; };
+    const auto ngroups = [&](int U) { return std::max<int64_t>(1, (nit + U - 1) / U); };
+    if (opt && membound) {
+        // HBM-bound launch with CTAs to spare: what matters is the bytes of
+        // staged regions in flight per SM (resident CTAs x stages), then
+        // resident warps. Few work units per thread keep the registers low
+        // enough for several CTAs per SM (launch bounds make ptxas hold them).
+        bd = 1;
+        double best = -1.0;
+        for (int U : {4, 2, 1}) {
+            if (U > nit) continue;
+            for (int Gx : {4, 3, 2, 1}) {
+                const int64_t G = std::min<int64_t>(Gx, ngroups(U));
+                const int64_t sbytes = G * rps(U) * stage_bytes;
+                if (sbytes > smem_cap) continue;
+                int64_t res = std::min<int64_t>({64 / std::max<int64_t>(1, warps), 32, (228 * 1024) / (sbytes + 1024),
+                                                 std::max<int64_t>(1, ctas / std::max<int64_t>(1, sms))});
+                const int64_t need = jit_regs_guess(K, sets(U) * K + p.num_coal_ilb + p.num_uncoal_ilb, U, 1) - 40;
+                while (res > 1 && need > 65536 / (res * warps * 32)) res--;
+                res = std::max<int64_t>(res, 1);
+                const double inflight = std::min(64.0 * 1024, (double)(res * sbytes));
+                const double score = inflight * 64.0 + (double)res * warps * 4.0 + U + (G >= 2 ? 1.0 : 0.0);
+                if (score > best) { best = score; bu = U; bs = (int)G; if (minb_out) *minb_out = (int)res; }
+            }
+        }
+        *U_out = bu;
+        *D_out = bd;
+        *S_out = bs;
+        return;
+    }
+    if (!opt && membound) {
+        // The baseline walks a thread's groups of U units as one stream of
+        // (group, step) slots with a D-slot load ring across group
+        // boundaries (lmt_jit.cuh), so D >= 2 keeps the next group's loads in
+        // flight; registers (launch bounds: several CTAs per SM) decide U.
+        const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
+        const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
+        auto est = [&](int U, int D) { return D * (sets(U) * K + ctx) + 3 * U + 30; };
+        const int cand[][2] = {{8, 2}, {4, 3}, {4, 2}, {2, 3}, {2, 2}, {1, 3}, {1, 2}};
+        bu = 1;
+        bd = 2;
+        for (auto &c : cand)
+            if (c[0] <= std::max<int64_t>(1, nit) && est(c[0], c[1]) <= regcap) { bu = c[0]; bd = c[1]; break; }
+        *U_out = bu;
+        *D_out = bd;
+        *S_out = 1;
+        return;
+    }
     if (!opt) {
         // start where the register estimate fits (ptxas has the last word in
         // JitCache::resolve; a good start saves the compiles of the step-down)
@@ -561,28 +615,27 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
             else { bu >>= 1; bd = 3; }
         }
     } else {
-        bd = 2;  // shared-memory loads: one step of lookahead covers them
+        bd = std::min(2, dmax);  // shared-memory loads: one step of lookahead covers them
         double best = -1.0;
         for (int U : {8, 4, 2, 1}) {
             if (U > nit) continue;
             const int64_t slot = sets(U) * K + p.num_coal_ilb + p.num_uncoal_ilb;
             const int64_t regs = std::min<int64_t>(jit_regs_guess(K, slot, U, 2), 65536 / maxt);
             const int64_t rregs = (regs + 7) / 8 * 8;
-            const bool sh = jit_share(A, U, regblock);
-            for (int Sx : {2 * U, U + 1, U}) {
-                if (Sx == U + 1 && (!sh || U == 1)) continue;
-                const int64_t S = std::min<int64_t>({(int64_t)Sx, kMaxStagesJ, std::max<int64_t>(nit, 1)});
-                if (S < U || S * stage_bytes > smem_cap) continue;
+            for (int Gx : {2, 1}) {
+                const int64_t G = std::min<int64_t>(Gx, ngroups(U));
+                const int64_t sbytes = G * rps(U) * stage_bytes;
+                if (sbytes > smem_cap) continue;
                 int64_t res = std::min<int64_t>(32, 64 / std::max<int64_t>(1, warps));
                 res = std::min<int64_t>(res, 65536 / std::max<int64_t>(1, rregs * warps * 32));
-                res = std::min<int64_t>(res, (228 * 1024) / (S * stage_bytes + 1024));
+                res = std::min<int64_t>(res, (228 * 1024) / (sbytes + 1024));
                 res = std::max<int64_t>(res, 1);
                 const int64_t act = std::min<int64_t>(res, (ctas + sms - 1) / sms);
                 const double chains = std::min(64.0, (double)act * (double)warps * U / 4.0);
-                // shared loads release U - 1 slots early (lmt_jit.cuh), so U + 1 slots overlap too
-                const bool overlap = S >= 2 * U || (sh && S >= U + 1);
+                // two stages: the next group's regions land while this one computes
+                const bool overlap = G >= 2 || ngroups(U) == 1;
                 const double score = chains * 64.0 + (overlap ? 16.0 : 0.0) + U * 2.0;
-                if (score > best) { best = score; bu = U; bs = (int)S; }
+                if (score > best) { best = score; bu = U; bs = (int)G; }
             }
         }
     }
@@ -598,8 +651,8 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
         while (bd > 1 && bd * step_instr(bu) > kLoopInstrBudget) bd--;
     }
     if (opt) {
-        bs = std::max(bs, bu);
-        while (bs > bu && (int64_t)bs * stage_bytes > smem_cap) bs--;
+        bs = std::max(bs, 1);
+        while (bs > 1 && (int64_t)bs * rps(bu) * stage_bytes > smem_cap) bs--;
     }
     *U_out = bu;
     *D_out = bd;
@@ -620,7 +673,7 @@ double launch_floor_s(const lmt_instance &p, int K, int64_t ctas, int64_t warps,
 }
 
 int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int32_t flags, const DevCtx *ctx,
-              Plan *pl) {
+              Plan *pl, const int32_t *tune = nullptr) {
     std::vector<std::string> v = violations(p);
     if (!v.empty()) {
         std::string m;
@@ -646,6 +699,9 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
     A.M = p.m;
     A.nwx = p.out_w / p.grid_x;
     A.nwy = p.out_h / p.grid_y;
+    A.nwx_shift = -1;
+    if (is_pow2(A.nwx))
+        for (A.nwx_shift = 0; (1 << A.nwx_shift) < A.nwx; A.nwx_shift++) {}
     const int64_t nm = (int64_t)p.n * p.m;
     A.ep_row0 = (int32_t)(nm % p.in_h);
     A.ep_col0 = (int32_t)(nm % p.in_w);
@@ -675,14 +731,16 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
         pl->wide = true;
     }
     const int64_t nrc = (rows + 255) / 256;
-    const int64_t bh = round_up((rows + nrc - 1) / nrc, 8);  // box stride stays 128-byte aligned
+    // one row chunk: the box is exactly the region's rows (no rows fetched
+    // that nobody reads); several: equal chunks whose stride stays 128-byte aligned
+    const int64_t bh = nrc == 1 ? rows : round_up((rows + nrc - 1) / nrc, 8);
     A.bw = (int32_t)bw;
     A.bh = (int32_t)bh;
     A.nrc = (int32_t)nrc;
     A.ncc = (int32_t)ncc;
-    const int64_t stage_floats = ncc * nrc * bh * bw;
-    A.stage_floats = (int32_t)stage_floats;
-    A.stage_bytes = (uint32_t)(stage_floats * 4);
+    const int64_t stage_tx = ncc * nrc * bh * bw;  // floats the TMA writes per region
+    A.stage_floats = (int32_t)round_up(stage_tx, 32);  // slot stride: slots start on 128-byte boundaries
+    A.stage_bytes = (uint32_t)(stage_tx * 4);
     const int64_t nit = (int64_t)A.nwx * A.nwy;
     const int64_t warps = ((int64_t)p.wg_x * p.wg_y + 31) / 32;
     const int64_t ctas = (int64_t)pl->grid.x * pl->grid.y;
@@ -715,17 +773,27 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
     // Baseline launches with few work units per thread (U <= 2) and CTAs to
     // spare get their ILP from resident warps instead: launch bounds that
     // keep 32 warps per SM resident (8 per scheduler) cap the registers.
+    // HBM-bound launches (the algorithmic bytes at HBM speed outlast the
+    // per-SM issue floor) with at least two full waves of CTAs are latency
+    // hidden by resident warps, not by work units in lockstep: a CTA loads,
+    // computes and stores its units once, so several CTAs per SM are what
+    // overlap one CTA's loads with another's stores.
+    const double chain_ops = (double)nm * (K + p.num_comp_ilb + p.num_coal_ilb + p.num_uncoal_ilb) +
+                             p.num_comp_ep + p.num_coal_ep + p.num_uncoal_ep;
+    const double issue_s = std::ceil((double)ctas / sms) * warps * (double)nit * chain_ops / 4.0 / 1.965e9;
+    const bool membound = pl->alg_bytes / 6.5e12 >= issue_s && ctas >= 2 * sms;
     int64_t maxt_b = maxt, minb = 1;
-    if (nit <= 2 && ctas >= 2 * sms) {
+    if ((nit <= 2 || membound) && ctas >= 2 * sms) {
         minb = std::min<int64_t>({(32 + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
                                   ctas / std::max<int64_t>(1, sms)});
         if (minb > 1) maxt_b = warps * 32;
         else minb = 1;
     }
-    int Ub, Db, Uo, Do, Sb, So;
-    choose_jit(K, p, A, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, regblock, &Ub, &Db, &Sb);
-    choose_jit(K, p, A, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_bytes, smem_cap, regblock, &Uo, &Do,
-               &So);
+    int Ub, Db, Uo, Do, Sb, So, minb_o = 1;
+    choose_jit(K, p, A, maxt_b * minb, ctas, warps, nit, sms, false, 0, smem_cap, regblock, membound, &Ub, &Db, &Sb,
+               nullptr);
+    choose_jit(K, p, A, maxt, ctas, warps, nit, sms, true, (int64_t)A.stage_floats * 4, smem_cap, regblock, membound, &Uo,
+               &Do, &So, &minb_o);
     pl->kb = k0;
     pl->kb.maxt = (int)maxt_b;
     pl->kb.minb = (int)minb;
@@ -739,10 +807,25 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
     pl->ko.opt = 1;
     pl->ko.share = jit_share(A, Uo, regblock) ? 1 : 0;
     pl->ko.wide = pl->wide ? 1 : 0;
+    if (tune) {  // explicit overrides (lmt_measure_opts.tune), for tuning studies
+        if (tune[0] > 0) pl->kb.U = std::min<int>(tune[0], 16);
+        if (tune[1] > 0) pl->kb.D = std::min(tune[1], 3);
+        if (tune[2] > 0) { pl->kb.minb = tune[2]; pl->kb.maxt = (int)(warps * 32); }
+        if (tune[3] > 0) pl->ko.U = std::min<int>(tune[3], 8);
+        if (tune[4] > 0) So = std::min<int>(tune[4], kMaxStagesJ);
+        if (tune[5] > 0) minb_o = tune[5];
+        if (pl->kb.share && !jit_share(A, pl->kb.U, regblock)) pl->kb.share = 0;
+        if (pl->ko.share && !jit_share(A, pl->ko.U, regblock)) pl->ko.share = 0;
+        while (So > 1 && (int64_t)So * (pl->ko.share ? 1 : pl->ko.U) * A.stage_floats * 4 > smem_cap) So--;
+    }
+    if (minb_o > 1) {  // launch bounds that keep minb_o CTAs of this size resident
+        pl->ko.minb = minb_o;
+        pl->ko.maxt = (int)(warps * 32);
+    }
     pl->in_copies = pl->kb.vec ? kInCopies : 1;
-    A.nstages = (int32_t)So;
-    pl->dyn_smem = (size_t)So * A.stage_bytes;
-    if ((int64_t)A.stage_bytes > smem_cap) pl->feasible = false;  // cannot stage even once on this device
+    A.nstages = (int32_t)So;  // group stages of the optimized variant's ring
+    pl->dyn_smem = (size_t)So * (pl->ko.share ? 1 : pl->ko.U) * A.stage_floats * 4;
+    if ((int64_t)A.stage_floats * 4 > smem_cap) pl->feasible = false;  // cannot stage even once on this device
     return LMT_OK;
 }
 
@@ -853,6 +936,7 @@ struct Batch {
     const float *const *h_in2;
     float *const *h_ob, *const *h_oo;
     lmt_measurement *out;
+    int32_t tune[6] = {0, 0, 0, 0, 0, 0};
     std::vector<Plan> plans;
     std::vector<char> ok, ran_base, ran_opt, filled;
     bool host() const { return h_in != nullptr; }
@@ -1167,7 +1251,7 @@ int measure_run(Batch &B) {
         if ((rc = compute_geometry(p, B.d, &g0))) { B.out[i].status = rc; continue; }
         const int64_t cols = B.host() ? B.h_cols[i] : g0.alloc_w;
         Plan &pl = B.plans[(size_t)i];
-        if ((rc = make_plan(p, B.d, round_up(cols, 4), B.flags, c, &pl))) { B.out[i].status = rc; continue; }
+        if ((rc = make_plan(p, B.d, round_up(cols, 4), B.flags, c, &pl, B.tune))) { B.out[i].status = rc; continue; }
         if (B.host() && (B.h_rows[i] < pl.g.alloc_h || B.h_cols[i] < pl.g.alloc_w)) {
             B.out[i].status = fail(LMT_ERR_ARG, "instance %lld: in too small", (long long)i);
             continue;
@@ -1402,12 +1486,13 @@ int lmt_measure_batch_ex(const lmt_instance *insts, int64_t n, const lmt_device 
     B.h_ob = h_out_base;
     B.h_oo = h_out_opt;
     B.out = out;
+    if (opts) memcpy(B.tune, opts->tune, sizeof B.tune);
     return measure_impl(B);
 }
 
 int lmt_measure_batch(const lmt_instance *insts, int64_t n, const lmt_device *dev, int32_t flags,
                       lmt_measurement *out) {
-    lmt_measure_opts o{flags, 0, nullptr, nullptr};
+    lmt_measure_opts o{flags, 0, nullptr, nullptr, {0, 0, 0, 0, 0, 0}};
     return lmt_measure_batch_ex(insts, n, dev, &o, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
 }
 
@@ -1416,7 +1501,7 @@ int lmt_measure_batch_host(const lmt_instance *insts, int64_t n, const lmt_devic
                            const float *const *h_in2, float *const *h_out_base, float *const *h_out_opt,
                            lmt_measurement *out) {
     if (!h_in || !in_rows || !in_cols || !h_in2) return fail(LMT_ERR_ARG, "host inputs required");
-    lmt_measure_opts o{flags, 0, nullptr, nullptr};
+    lmt_measure_opts o{flags, 0, nullptr, nullptr, {0, 0, 0, 0, 0, 0}};
     return lmt_measure_batch_ex(insts, n, dev, &o, h_in, in_rows, in_cols, h_in2, h_out_base, h_out_opt, out);
 }
 

@@ -398,6 +398,38 @@ __device__ __forceinline__ void consume(float (&acc)[NU_], const Slot<NU_> &s) {
         for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], s.w[k]);
 }
 
+// Epilogue context (codegen.py:227-237): the reads depend only on the
+// workitem (glin) and N*M, so a thread loads them once; the chain applies
+// comp_ep MADs, then the coal and uncoal values, per work unit.
+struct EpCtx {
+    float ce[NCE > 0 ? NCE : 1], ue[NUE > 0 ? NUE : 1];
+    __device__ __forceinline__ void load(const SynthArgs &A, const float *in2c, const float *in2u) {
+#pragma unroll
+        for (int k = 0; k < NCE; ++k) ce[k] = ctx_coal(A, in2c, in2c + (size_t)A.ep_row0 * P2, A.ep_row0, k);
+#if LMT_CTXWRAP
+#pragma unroll
+        for (int k = 0; k < NUE; ++k) ue[k] = ctx_uncoal(A, in2u, in2u + A.ep_col0, A.ep_col0, k);
+#else
+        uncoal_vec<NUE>(ue, in2u + A.ep_col0, A.ep_col0);
+#endif
+    }
+    template <int NU_>
+    __device__ __forceinline__ void apply(float (&acc)[NU_]) const {
+#pragma unroll
+        for (int k = 0; k < CE; ++k)
+#pragma unroll
+            for (int u = 0; u < NU_; ++u) acc[u] = __fmaf_rn(acc[u], mad_c1(CI + k), mad_c2(CI + k));
+#pragma unroll
+        for (int k = 0; k < NCE; ++k)
+#pragma unroll
+            for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], ce[k]);
+#pragma unroll
+        for (int k = 0; k < NUE; ++k)
+#pragma unroll
+            for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], ue[k]);
+    }
+};
+
 // NU_ work units of one thread: the full i/j nest then the epilogue.
 template <int NU_, class Src>
 __device__ __forceinline__ void run_units(const SynthArgs &A, Src src, const float *in2c, const float *in2u,
@@ -438,28 +470,9 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, Src src, const flo
             }
         }
     }
-    // epilogue (codegen.py:227-237): loads first, then the chain
-    float ce[NCE > 0 ? NCE : 1], ue[NUE > 0 ? NUE : 1];
-#pragma unroll
-    for (int k = 0; k < NCE; ++k) ce[k] = ctx_coal(A, in2c, in2c + (size_t)A.ep_row0 * P2, A.ep_row0, k);
-#if LMT_CTXWRAP
-#pragma unroll
-    for (int k = 0; k < NUE; ++k) ue[k] = ctx_uncoal(A, in2u, in2u + A.ep_col0, A.ep_col0, k);
-#else
-    uncoal_vec<NUE>(ue, in2u + A.ep_col0, A.ep_col0);
-#endif
-#pragma unroll
-    for (int k = 0; k < CE; ++k)
-#pragma unroll
-        for (int u = 0; u < NU_; ++u) acc[u] = __fmaf_rn(acc[u], mad_c1(CI + k), mad_c2(CI + k));
-#pragma unroll
-    for (int k = 0; k < NCE; ++k)
-#pragma unroll
-        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], ce[k]);
-#pragma unroll
-    for (int k = 0; k < NUE; ++k)
-#pragma unroll
-        for (int u = 0; u < NU_; ++u) acc[u] = __fadd_rn(acc[u], ue[k]);
+    EpCtx e;
+    e.load(A, in2c, in2u);
+    e.apply<NU_>(acc);
 }
 
 // ----------------------------------------------------- K1
@@ -475,36 +488,137 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB) lmt_kernel(cons
     const float *in2u = A.in2 + (size_t)(glin % H2) * P2;
     const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
     const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
-    const float *in0 = A.in + (A.pad * A.P + A.pad);
     const int nit = A.nwx * A.nwy;
-    int it = 0;
-    for (; it + U <= nit; it += U) {
-        GlobalSrc src;
-        src.pitch = A.P;
-        src.cs = A.in_copy;
-        size_t o[U];
+    // Work-unit iterations in order, ix fastest: iteration (ix, iy) reads
+    // home pointer prow + ix * sx of the row of work units iy (prow moves by
+    // sy per row) and writes orow + ix * wg_w -- no division per work unit.
+    const int sx = (A.a[0] * A.P + A.a[4]) * wg_w;
+    const long long sy = ((long long)A.a[1] * A.P + A.a[5]) * wg_h;
+    const float *prow = A.in + (A.pad * A.P + A.pad) +
+                        ((long long)(A.a[0] * wux0 + A.a[1] * wuy0) * A.P + A.a[4] * wux0 + A.a[5] * wuy0);
+    float *orow = A.out + ((size_t)wuy0 * A.out_w + wux0);
+    const size_t oy = (size_t)wg_h * A.out_w;
+    EpCtx ep;
+    ep.load(A, in2c, in2u);
+    // The thread's full groups of U work units as one stream of (group,
+    // step) slots: the D-slot load ring runs across group boundaries, so the
+    // loads of the next group are in flight while this one finishes and is
+    // stored (with N*M = 1 a group is a single step: without this every
+    // group would wait out a full memory latency on its own).
+    const int NM = A.N * A.M;
+    const int ng = nit / U;
+    const int total = ng * NM;
+    int fix = 0;  // fill cursor: column of work units and row pointer of the next group to load
+    const float *fprow = prow;
+    int cix = 0;  // consumer cursor: the group being accumulated
+    float *corow = orow;
+    GlobalSrc src;
+    src.pitch = A.P;
+    src.cs = A.in_copy;
+    Cursor q{0, in2c, 0, in2u, 0};
+    int ft = 0, fg = 0, ct = 0;
+    auto set_group = [&]() {  // src for the group at the fill cursor; cursor moves on by U units
+        if (fix + U <= A.nwx) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int ix = (it + u) % A.nwx, iy = (it + u) / A.nwx;
-            const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
-            src.p[u] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
-            o[u] = (size_t)wu_y * A.out_w + wu_x;
+            for (int u = 0; u < U; ++u) src.p[u] = fprow + (fix + u) * sx;
+            fix += U;
+            if (fix == A.nwx) {
+                fix = 0;
+                fprow += sy;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                src.p[u] = fprow + fix * sx;
+                if (++fix == A.nwx) {
+                    fix = 0;
+                    fprow += sy;
+                }
+            }
         }
-        float acc[U];
-        run_units<U>(A, src, in2c, in2u, acc);
+    };
+    auto fill_next = [&](Slot<U> &sl) {
+        fill<U>(sl, src, q, A, in2c, in2u);
+        if (++ft == NM) {
+            ft = 0;
+            if (++fg < ng) set_group();
+            q = Cursor{0, in2c, 0, in2u, 0};
+        } else {
+            advance<U>(q, src, A, in2c, in2u);
+        }
+    };
+    float acc[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) A.out[o[u]] = acc[u];
+    for (int u = 0; u < U; ++u) acc[u] = 0.0f;
+    auto consume_next = [&](const Slot<U> &sl) {
+        consume<U>(acc, sl);
+        if (++ct == NM) {  // the group's last step: epilogue, store, next group
+            ct = 0;
+            ep.apply<U>(acc);
+            if (cix + U <= A.nwx) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) corow[(cix + u) * wg_w] = acc[u];
+                cix += U;
+                if (cix == A.nwx) {
+                    cix = 0;
+                    corow += oy;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    corow[cix * wg_w] = acc[u];
+                    if (++cix == A.nwx) {
+                        cix = 0;
+                        corow += oy;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = 0.0f;
+        }
+    };
+    if (ng > 0) {
+        set_group();
+        Slot<U> sl[D];
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d)
+            if (d < total) fill_next(sl[d]);
+        int k = 0;
+        for (; k + 2 * D - 1 <= total; k += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                fill_next(sl[(d + D - 1) % D]);
+                consume_next(sl[d]);
+            }
+        }
+        for (; k < total; k += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                if (k + d < total) {
+                    if (k + d + D - 1 < total) fill_next(sl[(d + D - 1) % D]);
+                    consume_next(sl[d]);
+                }
+            }
+        }
     }
-    for (; it < nit; ++it) {
-        const int ix = it % A.nwx, iy = it / A.nwx;
-        const int wu_x = wux0 + ix * wg_w, wu_y = wuy0 + iy * wg_h;
-        GlobalSrc src;
-        src.pitch = A.P;
-        src.cs = A.in_copy;
-        src.p[0] = in0 + ((A.a[0] * wu_x + A.a[1] * wu_y) * A.P + A.a[4] * wu_x + A.a[5] * wu_y);
-        float acc[1];
-        run_units<1>(A, src, in2c, in2u, acc);
-        A.out[(size_t)wu_y * A.out_w + wu_x] = acc[0];
+    // the nit % U work units left over, one at a time
+    for (int it = ng * U; it < nit; ++it) {
+        GlobalSrc s1;
+        s1.pitch = A.P;
+        s1.cs = A.in_copy;
+        s1.p[0] = fprow + fix * sx;
+        float *o0 = corow + cix * wg_w;
+        if (++fix == A.nwx) {
+            fix = 0;
+            fprow += sy;
+        }
+        if (++cix == A.nwx) {
+            cix = 0;
+            corow += oy;
+        }
+        float a1[1];
+        run_units<1>(A, s1, in2c, in2u, a1);
+        *o0 = a1[0];
     }
 }
 #endif
@@ -512,67 +626,85 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB) lmt_kernel(cons
 // ----------------------------------------------------- K2
 
 #if LMT_OPT
-// Stage the region of work-unit iteration `it` into slot `slot` (the
-// cooperative copy of codegen.py:296-311, done by the TMA engine). The
-// innermost box coordinate must be 16-byte aligned, so the box starts at
-// org_col rounded down to 4 floats; region column 0 sits at (org_col & 3).
-__device__ __forceinline__ void stage_region(const SynthArgs &A, const TensorMap *map, float *smem,
-                                             unsigned long long *full, int slot, int it) {
-    const int ix = it % A.nwx, iy = it / A.nwx;
+// Work-unit iteration -> (ix, iy), ix fastest (kernel_model.py:158-170).
+__device__ __forceinline__ void iter_xy(const SynthArgs &A, int it, int &ix, int &iy) {
+    if (A.nwx_shift >= 0) {
+        ix = it & (A.nwx - 1);
+        iy = it >> A.nwx_shift;
+    } else {
+        ix = it % A.nwx;
+        iy = it / A.nwx;
+    }
+}
+
+// Regions staged per group of U work-unit iterations: one per unit, or one
+// for the whole group when its units read the same region (LMT_SHARE).
+constexpr int RPS = SHARE ? 1 : U;
+
+// Stage the region of work-unit iteration `it` at `dst` (the cooperative
+// copy of codegen.py:296-311, done by the TMA engine). The innermost box
+// coordinate must be 16-byte aligned, so the box starts at org_col rounded
+// down to 4 floats; region column 0 sits at (org_col & 3).
+__device__ __forceinline__ void stage_region(const SynthArgs &A, const TensorMap *map, float *dst,
+                                             unsigned long long *bar, int it) {
+    int ix, iy;
+    iter_xy(A, it, ix, iy);
     const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
     const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
     const int org_row = A.a[0] * wu_x0 + A.a[1] * wu_y0 + A.off_min_row + A.pad;
     const int org_col = (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & ~3;
-    float *dst = smem + slot * A.stage_floats;
-    mbar_expect_tx(&full[slot], A.stage_bytes);
     for (int cc = 0; cc < A.ncc; ++cc)
         for (int rc = 0; rc < A.nrc; ++rc)
-            tma_load_2d(dst + (cc * A.nrc + rc) * A.bh * A.bw, map, &full[slot], org_col + cc * A.bw,
-                        org_row + rc * A.bh);
+            tma_load_2d(dst + (cc * A.nrc + rc) * A.bh * A.bw, map, bar, org_col + cc * A.bw, org_row + rc * A.bh);
 }
 
-__device__ __forceinline__ int region_shift(const SynthArgs &A, int it) {
-    const int ix = it % A.nwx, iy = it / A.nwx;
-    const int wu_x0 = blockIdx.x * (blockDim.x * A.nwx) + ix * blockDim.x;
-    const int wu_y0 = blockIdx.y * (blockDim.y * A.nwy) + iy * blockDim.y;
-    return (A.a[4] * wu_x0 + A.a[5] * wu_y0 + A.off_min_col + A.pad) & 3;
+// Stage group g (iterations gU .. gU + cnt - 1) into group stage s: one
+// full barrier for all of its regions.
+__device__ __forceinline__ void stage_group(const SynthArgs &A, const TensorMap *map, float *smem,
+                                            unsigned long long *full, int s, int g, int nit) {
+    const int it0 = g * U;
+    const int nreg = SHARE ? 1 : min(U, nit - it0);
+    float *base = smem + (size_t)s * RPS * A.stage_floats;
+    mbar_expect_tx(&full[s], (unsigned)nreg * A.stage_bytes);
+    for (int r = 0; r < nreg; ++r) stage_region(A, map, base + r * A.stage_floats, &full[s], it0 + r);
 }
 
-// A warp is done with the slot of iteration `it`: arrive on its empty
-// barrier; whichever warp then sees the phase complete (the last to arrive,
-// or one that checks after it) and wins the claim re-arms the slot with
-// iteration it + S. No warp waits for another to reach a group boundary.
-__device__ __forceinline__ void release_slot(const SynthArgs &A, const TensorMap *map, float *smem,
-                                             unsigned long long *full, unsigned long long *empty, int *claim, int it,
-                                             int S, int nit) {
-    const int s = it % S;
+// A warp is done with group g: arrive on its stage's empty barrier;
+// whichever warp then sees the phase complete (the last to arrive, or one
+// that checks after it) and wins the claim re-arms the stage with group
+// g + G. No warp waits for another to reach a group boundary.
+__device__ __forceinline__ void release_group(const SynthArgs &A, const TensorMap *map, float *smem,
+                                              unsigned long long *full, unsigned long long *empty, int *claim, int g,
+                                              int G, int ngr, int nit) {
+    const int s = g % G;
     mbar_arrive(&empty[s]);
-    if (it + S < nit && mbar_test(&empty[s], (it / S) & 1) && atomicCAS(&claim[s], it, it + S) == it)
-        stage_region(A, map, smem, full, s, it + S);
+    if (g + G < ngr && mbar_test(&empty[s], (g / G) & 1) && atomicCAS(&claim[s], g, g + G) == g)
+        stage_group(A, map, smem, full, s, g + G, nit);
 }
 
-// Slots: iteration `it` lives in slot it % S and is re-armed for it + S as
-// soon as every warp released it (release_slot). With S >= 2U a group's
-// regions are in flight while the previous group computes. With LMT_SHARE
-// the group's U regions are identical: every unit reads the last unit's
-// slot and the other U - 1 are released as soon as they have landed, so
-// S >= U + 1 already overlaps the next group's staging with this group.
-extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
+// The ring holds G group stages (A.nstages); group g (U work-unit
+// iterations) lives in stage g % G behind one full and one empty mbarrier,
+// so a warp synchronises once per group, not once per work unit, and the
+// next G - 1 groups' regions are in flight while it computes. The consumer
+// walks the iterations in order with a cursor (ix, row pointers), so no
+// division runs per work unit.
+extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB)
     lmt_kernel(const __grid_constant__ TensorMap tmap, const SynthArgs A) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) unsigned long long full[kMaxStagesJ], empty[kMaxStagesJ];
-    __shared__ int claim[kMaxStagesJ];  // iteration slot s holds / was last armed for
+    __shared__ int claim[kMaxStagesJ];  // group stage s holds / was last armed for
 
     const int wi_x = threadIdx.x, wi_y = threadIdx.y;
     const int wg_w = blockDim.x, wg_h = blockDim.y;
     const int tid = wi_y * wg_w + wi_x;
     const int nwarps = (wg_w * wg_h + 31) >> 5;
     const int lane = tid & 31;
-    const int S = A.nstages;
+    const int G = A.nstages;
     const int nit = A.nwx * A.nwy;
+    const int ngr = (nit + U - 1) / U;
 
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < G; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], nwarps);
             claim[s] = s;
@@ -583,7 +715,7 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
     __syncthreads();
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tmap)) : "memory");
-        for (int s = 0; s < S && s < nit; ++s) stage_region(A, &tmap, smem, full, s, s);
+        for (int g = 0; g < G && g < ngr; ++g) stage_group(A, &tmap, smem, full, g, g, nit);
     }
     const int glin = (blockIdx.y * wg_h + wi_y) * A.grid_x + blockIdx.x * wg_w + wi_x;
     const float *in2c = A.in2 + (glin % W2);
@@ -594,9 +726,18 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
     const int hc0 = A.a[4] * wi_x + A.a[5] * wi_y - A.off_min_col;
     const int wux0 = blockIdx.x * (wg_w * A.nwx) + wi_x;
     const int wuy0 = blockIdx.y * (wg_h * A.nwy) + wi_y;
+    // region column shift of iteration (ix, iy): (cb + cx * ix + cy * iy) & 3
+    const int cb = A.a[4] * (blockIdx.x * wg_w * A.nwx) + A.a[5] * (blockIdx.y * wg_h * A.nwy) + A.off_min_col + A.pad;
+    const int cx = A.a[4] * wg_w, cy = A.a[5] * wg_h;
+    float *orow = A.out + ((size_t)wuy0 * A.out_w + wux0);
+    const size_t oy = (size_t)wg_h * A.out_w;
+    int ix = 0, iy = 0;  // cursor: the group's first iteration
 
-    for (int it0 = 0; it0 < nit;) {
-        const int cnt = (it0 + U <= nit) ? U : 1;
+    for (int g = 0; g < ngr; ++g) {
+        const int s = g % G;
+        const float *stage = smem + (size_t)s * RPS * A.stage_floats;
+        const int cnt = min(U, nit - g * U);
+        mbar_wait(&full[s], (g / G) & 1);
         if (cnt == U) {
 #if LMT_WIDE
             SmemWideSrc src;
@@ -605,58 +746,75 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, 1)
             SmemSrc src;
             src.pitch = A.bw;
 #endif
-            size_t o[U];
+            float *o[U];
+            int sh[U];
+            if (ix + U <= A.nwx) {  // the group lies in one row of work units
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    o[u] = orow + (ix + u) * wg_w;
+                    sh[u] = (cb + cx * (ix + u) + cy * iy) & 3;
+                }
+                ix += U;
+                if (ix == A.nwx) {
+                    ix = 0;
+                    ++iy;
+                    orow += oy;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    o[u] = orow + ix * wg_w;
+                    sh[u] = (cb + cx * ix + cy * iy) & 3;
+                    if (++ix == A.nwx) {
+                        ix = 0;
+                        ++iy;
+                        orow += oy;
+                    }
+                }
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int it = SHARE ? it0 + U - 1 : it0 + u;  // the slot this unit reads
-                mbar_wait(&full[(it0 + u) % S], ((it0 + u) / S) & 1);
-                const float *slot = smem + (it % S) * A.stage_floats;
+                const float *slot = stage + (SHARE ? 0 : u) * A.stage_floats;
 #if LMT_WIDE
                 src.slot[u] = slot;
                 src.hr[u] = hr0;
-                src.hc[u] = hc0 + region_shift(A, it);
+                src.hc[u] = hc0 + sh[u];
 #else
-                src.p[u] = slot + region_shift(A, it) + (hr0 * A.bw + hc0);
+                src.p[u] = slot + sh[u] + (hr0 * A.bw + hc0);
 #endif
-                const int ix = (it0 + u) % A.nwx, iy = (it0 + u) / A.nwx;
-                o[u] = (size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w);
-            }
-            if (SHARE) {  // the U - 1 regions nobody reads go back to the producer now
-                __syncwarp();
-                if (lane == 0)
-                    for (int q = 0; q < U - 1; ++q)
-                        release_slot(A, &tmap, smem, full, empty, claim, it0 + q, S, nit);
             }
             float acc[U];
             run_units<U>(A, src, in2c, in2u, acc);
 #pragma unroll
-            for (int u = 0; u < U; ++u) A.out[o[u]] = acc[u];
+            for (int u = 0; u < U; ++u) *o[u] = acc[u];
         } else {
-            const int it = it0;
-            mbar_wait(&full[it % S], (it / S) & 1);
-            const float *slot = smem + (it % S) * A.stage_floats;
+            for (int u = 0; u < cnt; ++u) {  // the last, short group: one unit at a time
+                const int sh0 = (cb + cx * ix + cy * iy) & 3;
+                float *o0 = orow + ix * wg_w;
+                if (++ix == A.nwx) {
+                    ix = 0;
+                    ++iy;
+                    orow += oy;
+                }
+                const float *slot = stage + (SHARE ? 0 : u) * A.stage_floats;
 #if LMT_WIDE
-            SmemWideSrc src;
-            src.chunk = A.nrc * A.bh * 256;
-            src.slot[0] = slot;
-            src.hr[0] = hr0;
-            src.hc[0] = hc0 + region_shift(A, it);
+                SmemWideSrc src;
+                src.chunk = A.nrc * A.bh * 256;
+                src.slot[0] = slot;
+                src.hr[0] = hr0;
+                src.hc[0] = hc0 + sh0;
 #else
-            SmemSrc src;
-            src.pitch = A.bw;
-            src.p[0] = slot + region_shift(A, it) + (hr0 * A.bw + hc0);
+                SmemSrc src;
+                src.pitch = A.bw;
+                src.p[0] = slot + sh0 + (hr0 * A.bw + hc0);
 #endif
-            float acc[1];
-            run_units<1>(A, src, in2c, in2u, acc);
-            const int ix = it % A.nwx, iy = it / A.nwx;
-            A.out[(size_t)(wuy0 + iy * wg_h) * A.out_w + (wux0 + ix * wg_w)] = acc[0];
+                float acc[1];
+                run_units<1>(A, src, in2c, in2u, acc);
+                *o0 = acc[0];
+            }
         }
         __syncwarp();
-        if (lane == 0) {
-            const int q0 = (SHARE && cnt == U) ? U - 1 : 0;
-            for (int q = q0; q < cnt; ++q) release_slot(A, &tmap, smem, full, empty, claim, it0 + q, S, nit);
-        }
-        it0 += cnt;
+        if (lane == 0) release_group(A, &tmap, smem, full, empty, claim, g, G, ngr, nit);
     }
 }
 #endif

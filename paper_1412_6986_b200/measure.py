@@ -121,18 +121,23 @@ def measure_raw(instances, dev=DEFAULT_DEVICE, *, chunk: int = 4096, **kw):
     return res
 
 
-def measure_records(records, dev=DEFAULT_DEVICE, *, samples: np.ndarray | None = None, **kw):
+def measure_records(records, dev=DEFAULT_DEVICE, *, samples: np.ndarray | None = None, tune=None, **kw):
     """Measure an int32 [n, 19] record table (sweep.InstanceTable.records);
     returns a numpy structured view of the lmt_measurement records. With
     ``samples`` (int64 [n, S] linear output indices) returns
     ``(records, values)``, values float32 [n, S, 2] = the baseline and
-    optimized output at those cells, for an independent (oracle) check."""
+    optimized output at those cells, for an independent (oracle) check.
+    ``tune``: kernel-shape overrides for tuning studies (lmt_measure_opts.tune:
+    baseline U, D, min CTAs/SM, optimized U, slots, min CTAs/SM; 0 = auto)."""
     from .sweep import records_to_c
 
     n = len(records)
     arr = records_to_c(records)
     out = (CMeasurement * max(n, 1))()
     opts = CMeasureOpts(measure_flags(**kw), 0, None, None)
+    if tune is not None:
+        for k, v in enumerate(list(tune)[:6]):
+            opts.tune[k] = int(v)
     vals = None
     if samples is not None:
         samples = np.ascontiguousarray(samples, dtype=np.int64).reshape(n, -1)

@@ -55,7 +55,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.CInstance) == 19 * 4
     assert ctypes.sizeof(_lib.CDevice) == 10 * 4
     assert ctypes.sizeof(_lib.CMeasurement) == 8 * 8 + 8 * 4
-    assert ctypes.sizeof(_lib.CMeasureOpts) == 4 + 4 + 8 + 8
+    assert ctypes.sizeof(_lib.CMeasureOpts) == 4 + 4 + 8 + 8 + 6 * 4 + 0  # + tune[6]
 
 
 def test_missing_library_fails_loudly(monkeypatch, tmp_path):
