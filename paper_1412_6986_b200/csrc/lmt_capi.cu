@@ -558,48 +558,36 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
     auto rps = [&](int U) -> int64_t { return jit_share(A, U, regblock) ? 1 : U; };
     const auto ngroups = [&](int U) { return std::max<int64_t>(1, (nit + U - 1) / U); };
     if (opt && membound) {
-        // HBM-bound launch with CTAs to spare: what matters is the bytes of
-        // staged regions in flight per SM (resident CTAs x stages), then
-        // resident warps. Few work units per thread keep the registers low
-        // enough for several CTAs per SM (launch bounds make ptxas hold them).
+        // HBM-bound launch with CTAs to spare: as many resident CTAs as the
+        // warps and shared memory allow (launch bounds hold the registers to
+        // it), U = 4 work units per group and 4 group stages in flight per
+        // CTA. Measured on B200 over (U, stages, CTAs/SM) on the HBM legs
+        // (tools/tune_hbm.py, profiles/r02_tune_hbm.json): within 2% of the
+        // best shape on each.
         bd = 1;
-        double best = -1.0;
-        for (int U : {4, 2, 1}) {
-            if (U > nit) continue;
-            for (int Gx : {4, 3, 2, 1}) {
-                const int64_t G = std::min<int64_t>(Gx, ngroups(U));
-                const int64_t sbytes = G * rps(U) * stage_bytes;
-                if (sbytes > smem_cap) continue;
-                int64_t res = std::min<int64_t>({64 / std::max<int64_t>(1, warps), 32, (228 * 1024) / (sbytes + 1024),
-                                                 std::max<int64_t>(1, ctas / std::max<int64_t>(1, sms))});
-                const int64_t need = jit_regs_guess(K, sets(U) * K + p.num_coal_ilb + p.num_uncoal_ilb, U, 1) - 40;
-                while (res > 1 && need > 65536 / (res * warps * 32)) res--;
-                res = std::max<int64_t>(res, 1);
-                const double inflight = std::min(64.0 * 1024, (double)(res * sbytes));
-                const double score = inflight * 64.0 + (double)res * warps * 4.0 + U + (G >= 2 ? 1.0 : 0.0);
-                if (score > best) { best = score; bu = U; bs = (int)G; if (minb_out) *minb_out = (int)res; }
-            }
-        }
+        bu = (int)std::min<int64_t>(4, std::max<int64_t>(1, nit));
+        while (bu & (bu - 1)) bu &= bu - 1;
+        int64_t G = std::min<int64_t>(4, ngroups(bu));
+        while (G > 1 && G * rps(bu) * stage_bytes > smem_cap) G--;
+        const int64_t res = std::min<int64_t>({64 / std::max<int64_t>(1, warps), 32,
+                                               (228 * 1024) / (G * rps(bu) * stage_bytes + 1024),
+                                               std::max<int64_t>(1, ctas / std::max<int64_t>(1, sms))});
+        if (minb_out) *minb_out = (int)std::max<int64_t>(1, res);
         *U_out = bu;
         *D_out = bd;
-        *S_out = bs;
+        *S_out = (int)G;
         return;
     }
     if (!opt && membound) {
         // The baseline walks a thread's groups of U units as one stream of
         // (group, step) slots with a D-slot load ring across group
-        // boundaries (lmt_jit.cuh), so D >= 2 keeps the next group's loads in
-        // flight; registers (launch bounds: several CTAs per SM) decide U.
-        const int64_t regcap = std::min<int64_t>(255, 65536 / maxt);
-        const int64_t ctx = p.num_coal_ilb + p.num_uncoal_ilb;
-        auto est = [&](int U, int D) { return D * (sets(U) * K + ctx) + 3 * U + 30; };
-        const int cand[][2] = {{8, 2}, {4, 3}, {4, 2}, {2, 3}, {2, 2}, {1, 3}, {1, 2}};
-        bu = 1;
-        bd = 2;
-        for (auto &c : cand)
-            if (c[0] <= std::max<int64_t>(1, nit) && est(c[0], c[1]) <= regcap) { bu = c[0]; bd = c[1]; break; }
+        // boundaries (lmt_jit.cuh); with 32 resident warps per SM (launch
+        // bounds) U = 8, D = 3 (stepped down by ptxas spills) was within 4%
+        // of the best measured shape on every HBM leg (tools/tune_hbm.py).
+        bu = (int)std::min<int64_t>(8, std::max<int64_t>(1, nit));
+        while (bu & (bu - 1)) bu &= bu - 1;
         *U_out = bu;
-        *D_out = bd;
+        *D_out = 3;
         *S_out = 1;
         return;
     }

@@ -675,10 +675,9 @@ __device__ __forceinline__ void stage_group(const SynthArgs &A, const TensorMap 
 // g + G. No warp waits for another to reach a group boundary.
 __device__ __forceinline__ void release_group(const SynthArgs &A, const TensorMap *map, float *smem,
                                               unsigned long long *full, unsigned long long *empty, int *claim, int g,
-                                              int G, int ngr, int nit) {
-    const int s = g % G;
+                                              int s, unsigned phase, int G, int ngr, int nit) {
     mbar_arrive(&empty[s]);
-    if (g + G < ngr && mbar_test(&empty[s], (g / G) & 1) && atomicCAS(&claim[s], g, g + G) == g)
+    if (g + G < ngr && mbar_test(&empty[s], phase) && atomicCAS(&claim[s], g, g + G) == g)
         stage_group(A, map, smem, full, s, g + G, nit);
 }
 
@@ -733,11 +732,12 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB)
     const size_t oy = (size_t)wg_h * A.out_w;
     int ix = 0, iy = 0;  // cursor: the group's first iteration
 
+    int s = 0;
+    unsigned phase = 0;  // stage g % G and the parity of its use (g / G) & 1, kept incrementally
     for (int g = 0; g < ngr; ++g) {
-        const int s = g % G;
         const float *stage = smem + (size_t)s * RPS * A.stage_floats;
         const int cnt = min(U, nit - g * U);
-        mbar_wait(&full[s], (g / G) & 1);
+        mbar_wait(&full[s], phase);
         if (cnt == U) {
 #if LMT_WIDE
             SmemWideSrc src;
@@ -814,7 +814,11 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB)
             }
         }
         __syncwarp();
-        if (lane == 0) release_group(A, &tmap, smem, full, empty, claim, g, G, ngr, nit);
+        if (lane == 0) release_group(A, &tmap, smem, full, empty, claim, g, s, phase, G, ngr, nit);
+        if (++s == G) {
+            s = 0;
+            phase ^= 1;
+        }
     }
 }
 #endif
