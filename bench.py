@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--no-hbm", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump", default=None, help="save per-instance records and measurements (npz)")
+    ap.add_argument("--verify-sweep", default=None, metavar="DIR",
+                    help="no benchmark: check the sampled output cells a run_sweep --samples job wrote under DIR "
+                         "against the CPU oracle and print one JSON summary")
     return ap.parse_args()
 
 
@@ -82,23 +85,10 @@ def global_rows(seed: int, n_total: int, step: int, world: int, batch: int) -> n
 
 
 def sample_cells(rec: np.ndarray, S: int, seed: int) -> np.ndarray:
-    """int64 [n, S] output cells per instance for the oracle check: four
-    cells of workgroup 0's first work-unit iteration, four of its last, the
-    last cell of the output, and the rest uniform over the output."""
-    rng = np.random.default_rng(seed)
-    out = np.empty((len(rec), S), dtype=np.int64)
-    for i, r in enumerate(np.asarray(rec, dtype=np.int64)):
-        oh, ow, gx, gy, wx, wy = r[2], r[3], r[15], r[16], r[17], r[18]
-        nwx, nwy = ow // gx, oh // gy
-        first = [(0, 0), (0, wx - 1), (wy - 1, 0), (wy - 1, wx - 1)]
-        ly, lx = (nwy - 1) * wy, (nwx - 1) * wx
-        last = [(ly, lx), (ly, lx + wx - 1), (ly + wy - 1, lx), (ly + wy - 1, lx + wx - 1)]
-        fixed = [y * ow + x for y, x in first + last] + [oh * ow - 1]
-        k = min(len(fixed), S)
-        out[i, :k] = fixed[:k]
-        if S > k:
-            out[i, k:] = rng.integers(0, oh * ow, size=S - k)
-    return out
+    """The output cells read back per instance (sweep.sample_cells)."""
+    from paper_1412_6986_b200.sweep import sample_cells as sc
+
+    return sc(rec, S, seed)
 
 
 def oracle_check(rec: np.ndarray, res: np.ndarray, idx: np.ndarray, vals: np.ndarray) -> dict:
@@ -718,8 +708,31 @@ def run_e2e(args, L, table, steps_rows, mode, world, rank, barrier, gather_max_s
                     "H2D of in/in2 and D2H of both outputs per instance inside the timed region)"}
 
 
+def verify_sweep(out_dir: str) -> dict:
+    """Every instance of a measured sweep (run_sweep --samples) against the
+    CPU oracle: the sampled cells of both variants, bitwise."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(out_dir, "rank*", "chunk*.npz")))
+    tot = {"chunks": len(files), "instances": 0, "mismatched": 0, "cells": 0, "bad_rows": [], "seconds": 0.0}
+    for f in files:
+        z = np.load(f)
+        if "sample_idx" not in z:
+            continue
+        d = oracle_check(z["rec"], z["res"], z["sample_idx"], z["sample_vals"])
+        tot["instances"] += d["instances"]
+        tot["mismatched"] += d["mismatched"]
+        tot["cells"] += d["cells"]
+        tot["seconds"] += d["seconds"]
+        tot["bad_rows"] += [int(z["rows"][i]) for i in d["bad"]][: max(0, 16 - len(tot["bad_rows"]))]
+    return tot
+
+
 def main():
     args = parse()
+    if args.verify_sweep:
+        print(json.dumps(verify_sweep(args.verify_sweep)), flush=True)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

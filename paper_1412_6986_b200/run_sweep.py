@@ -40,15 +40,25 @@ def _args(argv=None):
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl with a GPU, else gloo)")
     ap.add_argument("--study", action="store_true",
                     help="after the gather: the paper's RF study on modelled and measured labels (study.py)")
+    ap.add_argument("--family", default="all", choices=("all", "dla", "grid"),
+                    help="restrict to the dense-linear-algebra or structured-grid patterns (sweep.DLA_FAMILY / "
+                         "GRID_FAMILY)")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="launches of <= 74 CTAs in disjoint SM partitions (the bench's placement)")
+    ap.add_argument("--samples", type=int, default=0,
+                    help="output cells per instance read back into the chunk files (sweep.sample_cells), so an "
+                         "independent checker can compare them with the CPU reference")
     return ap.parse_args(argv)
 
 
-def rank_share(table, world: int, rank: int, sample: int = 0, seed: int = 0) -> np.ndarray:
-    """Cost-balanced disjoint share of the whole selection, or of a seeded
-    random subset of `sample` rows (sorted rows)."""
+def rank_share(table, world: int, rank: int, sample: int = 0, seed: int = 0, family: str = "all") -> np.ndarray:
+    """Cost-balanced disjoint share of the whole selection (or of one pattern
+    family), or of a seeded random subset of `sample` rows (sorted rows)."""
     from . import sweep
 
     rows = np.arange(len(table))
+    if family != "all":
+        rows = sweep.family_rows(table, sweep.DLA_FAMILY if family == "dla" else sweep.GRID_FAMILY)
     if sample and sample < len(rows):
         rows = np.sort(np.random.default_rng(seed ^ 0x5A3B1E).choice(len(rows), size=sample, replace=False))
     if world == 1:
@@ -78,7 +88,7 @@ def run(argv=None) -> dict:
 
     spec = sweep.SamplingSpec(max_instances=args.max_instances, seed=args.seed)
     table = sweep.select_instance_table(spec)
-    mine = rank_share(table, world, rank, args.sample, args.seed)
+    mine = rank_share(table, world, rank, args.sample, args.seed, args.family)
     if args.limit:
         mine = mine[: args.limit]
     rdir = os.path.join(args.out, f"rank{rank:03d}")
@@ -86,7 +96,8 @@ def run(argv=None) -> dict:
     t0 = time.time()
     rec = table.records(mine)
     fb = features_records(rec)
-    measure.prepare_records(rec)
+    mode = dict(concurrent=args.concurrent)
+    measure.prepare_records(rec, **mode)
     t_prep = time.time() - t0
 
     # ---- chunks with checkpoint/resume
@@ -102,11 +113,18 @@ def run(argv=None) -> dict:
                 done_res.append(z["res"])
                 resumed += 1
                 continue
+        crec = table.records(rows)
+        extra = {}
         t1 = time.time()
-        res = measure.measure_records(table.records(rows))
+        if args.samples:
+            idx = sweep.sample_cells(crec, args.samples, args.seed * 1_000_003 + k)
+            res, vals = measure.measure_records(crec, samples=idx, **mode)
+            extra = dict(sample_idx=idx, sample_vals=vals)
+        else:
+            res = measure.measure_records(crec, **mode)
         t_meas += time.time() - t1
         tmp = path + ".tmp.npz"
-        np.savez(tmp, rows=rows, res=res)
+        np.savez(tmp, rows=rows, res=res, rec=crec, **extra)
         os.replace(tmp, path)
         done_rows.append(rows)
         done_res.append(res)
@@ -125,8 +143,10 @@ def run(argv=None) -> dict:
     extra = np.stack([res_all["mismatches"].astype(np.float64), res_all["status"].astype(np.float64)], 1)
     labels = ldist.all_gather_labels(np.concatenate([lab, extra], 1), device=device)
     summary = {"rank": rank, "world": world, "max_instances": args.max_instances, "seed": args.seed,
+               "family": args.family, "sample": args.sample, "concurrent": args.concurrent,
                "rows": int(len(mine)), "chunks_resumed": resumed,
                "prepare_s": t_prep, "measure_s": t_meas,
+               "instances_per_s": (len(mine) - resumed * args.chunk) / t_meas if t_meas > 0 else None,
                "mismatched": int((res_all["mismatches"] > 0).sum()),
                "verified": int((res_all["mismatches"] == 0).sum())}
     if args.study:  # every rank trains the same forests, predicts the held-out rows it measured

@@ -350,3 +350,24 @@ def records_to_c(records: np.ndarray):
     if len(rec):
         ctypes.memmove(arr, rec.ctypes.data, rec.nbytes)
     return arr
+
+
+def sample_cells(rec: np.ndarray, S: int, seed: int) -> np.ndarray:
+    """int64 [n, S] output cells per instance to read back for an
+    independent check against the CPU reference: four cells of workgroup 0's
+    first work-unit iteration, four of its last, the last cell of the output,
+    and the rest uniform over the output."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((len(rec), S), dtype=np.int64)
+    for i, r in enumerate(np.asarray(rec, dtype=np.int64)):
+        oh, ow, gx, gy, wx, wy = r[2], r[3], r[15], r[16], r[17], r[18]
+        nwx, nwy = ow // gx, oh // gy
+        first = [(0, 0), (0, wx - 1), (wy - 1, 0), (wy - 1, wx - 1)]
+        ly, lx = (nwy - 1) * wy, (nwx - 1) * wx
+        last = [(ly, lx), (ly, lx + wx - 1), (ly + wy - 1, lx), (ly + wy - 1, lx + wx - 1)]
+        fixed = [y * ow + x for y, x in first + last] + [oh * ow - 1]
+        k = min(len(fixed), S)
+        out[i, :k] = fixed[:k]
+        if S > k:
+            out[i, k:] = rng.integers(0, oh * ow, size=S - k)
+    return out
