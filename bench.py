@@ -84,6 +84,37 @@ def global_rows(seed: int, n_total: int, step: int, world: int, batch: int) -> n
     return np.sort(g)
 
 
+def step_rows(table, seed: int, step: int, world: int, rank: int, batch: int) -> np.ndarray:
+    """This rank's rows of step `step`: the global batch split into
+    contiguous ranges of equal estimated cost (sweep.shard_contiguous on the
+    sorted batch). Every rank computes every rank's share the
+    same way, so shard sizes need no communication."""
+    from paper_1412_6986_b200 import sweep
+
+    g = global_rows(seed, len(table), step, world, batch)
+    if world == 1:
+        return g
+    cost = sweep.launch_cost(table.records(g))
+    return g[sweep.shard_contiguous(cost, world)[rank]]
+
+
+def max_sum_over_ranks(vals_max, vals_sum, world: int, group=None):
+    """Timers (max over ranks) and counters (sum) through the host-side gloo
+    group: they stay off NVLink; the label all-gather is the only NCCL
+    collective."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return list(vals_max), list(vals_sum)
+    t = torch.tensor(list(vals_max) + list(vals_sum), dtype=torch.float64)
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    st = torch.stack(parts)
+    nm = len(vals_max)
+    return st[:, :nm].max(0).values.tolist(), st[:, nm:].sum(0).tolist()
+
+
 def sample_cells(rec: np.ndarray, S: int, seed: int) -> np.ndarray:
     """The output cells read back per instance (sweep.sample_cells)."""
     from paper_1412_6986_b200.sweep import sample_cells as sc
@@ -320,21 +351,10 @@ def run_ours(args, rank: int, world: int, local_rank: int, meta_group):
             dist.barrier(group=meta_group)
 
     def my_rows(step):
-        g = global_rows(args.seed, len(table), step, world, args.batch)
-        if world == 1:
-            return g
-        cost = L.sweep.launch_cost(table.records(g))
-        return g[L.sweep.shard_contiguous(cost, world)[rank]]
+        return step_rows(table, args.seed, step, world, rank, args.batch)
 
     def gather_max_sum(vals_max, vals_sum):
-        t = torch.tensor(list(vals_max) + list(vals_sum), dtype=torch.float64)
-        if world > 1:
-            parts = [torch.zeros_like(t) for _ in range(world)]
-            dist.all_gather(parts, t, group=meta_group)
-            st = torch.stack(parts)
-            nm = len(vals_max)
-            return st[:, :nm].max(0).values.tolist(), st[:, nm:].sum(0).tolist()
-        return list(vals_max), list(vals_sum)
+        return max_sum_over_ranks(vals_max, vals_sum, world, meta_group)
 
     # compile + load every specialised kernel the run will launch (NVRTC,
     # sm_100a; the reference's per-kernel compile step), before any timing
@@ -376,7 +396,10 @@ def run_ours(args, rank: int, world: int, local_rank: int, meta_group):
     orc = oracle_check(rec_all, res_all, idx_all, vals_all)
 
     # ---- labels: NCCL all-gather of (row, t_base, t_opt) -- the only NCCL collective
-    labels = L.dist.all_gather_labels(L.dist.label_matrix(rows_all, res_all), device=COLL)
+    # every rank's share size is known locally (deterministic sharding): one all-gather, no size exchange
+    sizes = [sum(len(step_rows(table, args.seed, s, world, r, args.batch))
+                 for s in range(args.warmup, args.warmup + args.steps)) for r in range(world)]
+    labels = L.dist.all_gather_labels(L.dist.label_matrix(rows_all, res_all), device=COLL, sizes=sizes)
     n_labels = int(labels.shape[0])
     ok = res_all["t_base_ms"] > 0
     ran_opt = res_all["t_opt_ms"] > 0

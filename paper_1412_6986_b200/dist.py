@@ -36,10 +36,11 @@ def label_matrix(rows: np.ndarray, res: np.ndarray) -> np.ndarray:
                      res["t_opt_ms"].astype(np.float64)], axis=1)
 
 
-def all_gather_labels(labels: np.ndarray, device=None, group=None) -> np.ndarray:
-    """All-gather variable-length [n_r, 3] label blocks from every rank and
-    return them sorted by row. One size exchange plus one all-gather of the
-    padded blocks."""
+def all_gather_labels(labels: np.ndarray, device=None, group=None, sizes=None) -> np.ndarray:
+    """All-gather variable-length [n_r, k] label blocks from every rank and
+    return them sorted by row: one all-gather of blocks padded to the
+    largest. ``sizes`` (rows per rank) is known to every rank when the
+    sharding is deterministic; without it the sizes are exchanged first."""
     import torch
     import torch.distributed as dist
 
@@ -48,13 +49,18 @@ def all_gather_labels(labels: np.ndarray, device=None, group=None) -> np.ndarray
         out = lab.cpu().numpy()
         return out[np.argsort(out[:, 0], kind="stable")]
     world = dist.get_world_size(group)
-    n = torch.tensor([lab.shape[0]], dtype=torch.int64, device=device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    mx = int(max(int(s.item()) for s in sizes))
+    if sizes is None:
+        n = torch.tensor([lab.shape[0]], dtype=torch.int64, device=device)
+        got = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(got, n, group=group)
+        sizes = [int(s.item()) for s in got]
+    sizes = [int(s) for s in sizes]
+    if len(sizes) != world or sizes[dist.get_rank(group)] != lab.shape[0]:
+        raise ValueError(f"label block sizes {sizes} do not match this rank's {lab.shape[0]} rows")
+    mx = max(sizes)
     pad = torch.zeros((mx, lab.shape[1]), dtype=torch.float64, device=device)
     pad[: lab.shape[0]] = lab
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
-    out = torch.cat([b[: int(s.item())] for b, s in zip(bufs, sizes)]).cpu().numpy()
+    out = torch.cat([b[:s] for b, s in zip(bufs, sizes)]).cpu().numpy()
     return out[np.argsort(out[:, 0], kind="stable")]

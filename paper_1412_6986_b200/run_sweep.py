@@ -141,7 +141,10 @@ def run(argv=None) -> dict:
     # ---- the only collective: measured labels
     lab = ldist.label_matrix(rows_all, res_all)
     extra = np.stack([res_all["mismatches"].astype(np.float64), res_all["status"].astype(np.float64)], 1)
-    labels = ldist.all_gather_labels(np.concatenate([lab, extra], 1), device=device)
+    # every rank's share is a deterministic function of the selection: sizes need no exchange
+    sizes = [len(rank_share(table, world, r, args.sample, args.seed, args.family)[: args.limit or None])
+             for r in range(world)]
+    labels = ldist.all_gather_labels(np.concatenate([lab, extra], 1), device=device, sizes=sizes)
     summary = {"rank": rank, "world": world, "max_instances": args.max_instances, "seed": args.seed,
                "family": args.family, "sample": args.sample, "concurrent": args.concurrent,
                "rows": int(len(mine)), "chunks_resumed": resumed,

@@ -136,3 +136,55 @@ def test_two_rank_study_matches_one_rank(tmp_path):
     assert a["held_out"] == 360 and a["train"] == 40
     for k in ("modelled_labels", "measured_labels"):
         assert 0.0 <= a[k]["count_accuracy"] <= 1.0 and sum(a[k]["confusion"]) == 360
+
+
+def _bench_worker(rank, world, port, out_dir):
+    """bench.py's multi-rank plumbing with stand-in measurements: per step
+    the contiguous cost-prefix share (bench.step_rows), the label all-gather
+    with locally known sizes (the only data collective; gloo here, NCCL on
+    GPUs) and timers/counters through a separate gloo group."""
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import bench
+    import paper_1412_6986_b200 as L
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    meta = dist.new_group(backend="gloo")
+    try:
+        table = L.select_instance_table(L.SamplingSpec(max_instances=20_000, seed=0))
+        steps, batch = range(1, 3), 24
+        mine = np.concatenate([bench.step_rows(table, 0, s, world, rank, batch) for s in steps])
+        sizes = [sum(len(bench.step_rows(table, 0, s, world, r, batch)) for s in steps) for r in range(world)]
+        res = np.zeros(len(mine), dtype=L.measure.MEASUREMENT_DTYPE)
+        res["t_base_ms"] = mine * 0.5 + 1.0
+        res["t_opt_ms"] = np.where(mine % 3 == 0, -1.0, mine * 0.25 + 2.0)
+        labels = L.dist.all_gather_labels(L.dist.label_matrix(mine, res), sizes=sizes)
+        (mx,), (n,) = bench.max_sum_over_ranks([float(rank)], [len(mine)], world, meta)
+        glob = np.concatenate([bench.global_rows(0, len(table), s, world, batch) for s in steps])
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), mine=mine, labels=labels, mx=mx, n=n, glob=glob)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_bench_sharding_and_gather(tmp_path, world):
+    pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_bench_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    mine = [g["mine"] for g in got]
+    glob = got[0]["glob"]
+    allm = np.concatenate(mine)
+    assert len(np.unique(allm)) == len(allm) == len(glob)  # disjoint
+    assert np.array_equal(np.sort(allm), np.sort(glob))    # complete
+    for g in got:
+        lab = g["labels"]
+        r = lab[:, 0]
+        assert np.array_equal(r, np.sort(glob).astype(np.float64))
+        assert np.array_equal(lab[:, 1], r * 0.5 + 1.0)
+        assert np.array_equal(lab[:, 2], np.where(r % 3 == 0, -1.0, r * 0.25 + 2.0))
+        assert g["mx"] == world - 1 and g["n"] == len(glob)
