@@ -49,41 +49,77 @@ __global__ void k_transpose_opt(const float *__restrict__ A, float *__restrict__
 // ------------------------------------------------------------ matrixMul
 // C = A x B, n x n. CTA = T x T outputs, blockDim (T, T / W): thread (tx, ty)
 // computes rows ty + r * (T / W), r < W, column tx. acc = fmaf(A[i][k], B[k][j], acc), k ascending.
+// Both variants take k four at a time: one 128-bit read of A[row][k .. k+3]
+// per row (the same address across the warp: a broadcast) feeds 4 FMAs per
+// output, so the W rows' 4W FMAs cost W + 4 loads instead of 2 per FMA.
 __global__ void k_matmul_base(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
                               int n, int T, int W) {
     const int h = T / W;
     const int col = blockIdx.x * T + threadIdx.x;
     for (int r = 0; r < W; ++r) {
         const int row = blockIdx.y * T + threadIdx.y + r * h;
+        const float *ar = A + (size_t)row * n;
         float acc = 0.0f;
-        for (int k = 0; k < n; ++k) acc = __fmaf_rn(A[(size_t)row * n + k], B[(size_t)k * n + col], acc);
+        if ((n & 3) == 0) {
+            for (int k = 0; k < n; k += 4) {
+                const float4 a = __ldg(reinterpret_cast<const float4 *>(ar + k));
+                acc = __fmaf_rn(a.x, __ldg(B + (size_t)(k + 0) * n + col), acc);
+                acc = __fmaf_rn(a.y, __ldg(B + (size_t)(k + 1) * n + col), acc);
+                acc = __fmaf_rn(a.z, __ldg(B + (size_t)(k + 2) * n + col), acc);
+                acc = __fmaf_rn(a.w, __ldg(B + (size_t)(k + 3) * n + col), acc);
+            }
+        } else {
+            for (int k = 0; k < n; ++k) acc = __fmaf_rn(ar[k], B[(size_t)k * n + col], acc);
+        }
         C[(size_t)row * n + col] = acc;
     }
 }
 
+// optimized: A and B tiles staged in shared memory (As rows padded to T + 4
+// floats: 16-byte aligned for the 128-bit k reads), the next tiles' elements
+// loaded into registers while the current tiles are consumed.
 template <int W>
 __global__ void k_matmul_opt(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
                              int n, int T) {
-    extern __shared__ float sm[];  // As[T][T + 1], Bs[T][T + 1]
-    const int P = T + 1, h = T / W;
-    float *As = sm, *Bs = sm + T * P;
+    extern __shared__ __align__(16) float sm[];  // As[T][T + 4], Bs[T][T]
+    const int PA = T + 4, h = T / W;
+    float *As = sm, *Bs = sm + T * PA;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int col = blockIdx.x * T + tx;
-    float acc[W];
+    const size_t arow0 = (size_t)(blockIdx.y * T) * n;
+    float acc[W], ra[W], rb[W];
 #pragma unroll
-    for (int r = 0; r < W; ++r) acc[r] = 0.0f;
+    for (int r = 0; r < W; ++r) {
+        acc[r] = 0.0f;
+        ra[r] = A[arow0 + (size_t)(ty + r * h) * n + tx];
+        rb[r] = B[(size_t)(ty + r * h) * n + col];
+    }
     for (int k0 = 0; k0 < n; k0 += T) {
 #pragma unroll
         for (int r = 0; r < W; ++r) {
             const int lr = ty + r * h;
-            As[lr * P + tx] = A[(size_t)(blockIdx.y * T + lr) * n + k0 + tx];
-            Bs[lr * P + tx] = B[(size_t)(k0 + lr) * n + col];
+            As[lr * PA + tx] = ra[r];
+            Bs[lr * T + tx] = rb[r];
         }
         __syncthreads();
-        for (int kk = 0; kk < T; ++kk) {
-            const float b = Bs[kk * P + tx];
+        if (k0 + T < n) {
 #pragma unroll
-            for (int r = 0; r < W; ++r) acc[r] = __fmaf_rn(As[(ty + r * h) * P + kk], b, acc[r]);
+            for (int r = 0; r < W; ++r) {
+                ra[r] = __ldg(A + arow0 + (size_t)(ty + r * h) * n + k0 + T + tx);
+                rb[r] = __ldg(B + (size_t)(k0 + T + ty + r * h) * n + col);
+            }
+        }
+        for (int kk = 0; kk < T; kk += 4) {
+            const float b0 = Bs[(kk + 0) * T + tx], b1 = Bs[(kk + 1) * T + tx];
+            const float b2 = Bs[(kk + 2) * T + tx], b3 = Bs[(kk + 3) * T + tx];
+#pragma unroll
+            for (int r = 0; r < W; ++r) {
+                const float4 a = *reinterpret_cast<const float4 *>(As + (ty + r * h) * PA + kk);
+                acc[r] = __fmaf_rn(a.x, b0, acc[r]);
+                acc[r] = __fmaf_rn(a.y, b1, acc[r]);
+                acc[r] = __fmaf_rn(a.z, b2, acc[r]);
+                acc[r] = __fmaf_rn(a.w, b3, acc[r]);
+            }
         }
         __syncthreads();
     }
@@ -167,67 +203,207 @@ __global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict_
 
 // ------------------------------------------------------------ MVT (Polybench)
 // x1[i] = x1_0[i] + sum_j A[i][j] * y1[j];  x2[i] = x2_0[i] + sum_j A[j][i] * y2[j]  (j ascending)
-__global__ void k_mvt1_base(const float *__restrict__ A, const float *__restrict__ y1, const float *__restrict__ x1_0,
-                            float *__restrict__ x1, int n) {
+//
+// n x n A is 64 MB at n = 4096 while only n threads carry a chain each, so
+// what bounds both kernels is the bytes in flight per thread, not the
+// arithmetic: the baselines read 128-bit (row walk) or coalesced (column
+// walk) with the next loads issued before the current chain step; the
+// optimized variants stream A through a TMA ring in shared memory.
+
+// baseline kernel 1: thread i walks row i, four j per 128-bit load, eight loads in flight
+__global__ void __launch_bounds__(512) k_mvt1_base(const float *__restrict__ A, const float *__restrict__ y1,
+                                                   const float *__restrict__ x1_0, float *__restrict__ x1, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     float acc = x1_0[i];
-    for (int j = 0; j < n; ++j) acc = __fmaf_rn(A[(size_t)i * n + j], y1[j], acc);  // row walk per thread
+    const float *row = A + (size_t)i * n;
+    if ((n & 3) == 0) {
+        const float4 *a4 = reinterpret_cast<const float4 *>(row);
+        const float4 *y4 = reinterpret_cast<const float4 *>(y1);
+        const int n4 = n >> 2;
+        int q = 0;
+        for (; q + 8 <= n4; q += 8) {
+            float4 a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = __ldg(a4 + q + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float4 y = __ldg(y4 + q + u);
+                acc = __fmaf_rn(a[u].x, y.x, acc);
+                acc = __fmaf_rn(a[u].y, y.y, acc);
+                acc = __fmaf_rn(a[u].z, y.z, acc);
+                acc = __fmaf_rn(a[u].w, y.w, acc);
+            }
+        }
+        for (int j = q * 4; j < n; ++j) acc = __fmaf_rn(row[j], y1[j], acc);
+    } else {
+        for (int j = 0; j < n; ++j) acc = __fmaf_rn(row[j], y1[j], acc);
+    }
     x1[i] = acc;
 }
 
-__global__ void k_mvt2_base(const float *__restrict__ A, const float *__restrict__ y2, const float *__restrict__ x2_0,
-                            float *__restrict__ x2, int n) {
+// baseline kernel 2: thread i walks column i (coalesced across the warp), 16 rows in flight
+__global__ void __launch_bounds__(512) k_mvt2_base(const float *__restrict__ A, const float *__restrict__ y2,
+                                                   const float *__restrict__ x2_0, float *__restrict__ x2, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     float acc = x2_0[i];
-    for (int j = 0; j < n; ++j) acc = __fmaf_rn(A[(size_t)j * n + i], y2[j], acc);  // coalesced across threads
+    int j = 0;
+    for (; j + 16 <= n; j += 16) {
+        float a[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a[u] = __ldg(A + (size_t)(j + u) * n + i);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = __fmaf_rn(a[u], __ldg(y2 + j + u), acc);
+    }
+    for (; j < n; ++j) acc = __fmaf_rn(A[(size_t)j * n + i], y2[j], acc);
     x2[i] = acc;
 }
 
-// optimized kernel 1: a [wg][T] tile of A (loaded along rows: coalesced) and
-// T entries of y1 staged per step
-__global__ void k_mvt1_opt(const float *__restrict__ A, const float *__restrict__ y1, const float *__restrict__ x1_0,
-                           float *__restrict__ x1, int n, int T) {
-    extern __shared__ float s[];  // sA[wg][T + 1], sy[T]
-    const int wg = blockDim.x, P = T + 1;
-    float *sA = s, *sy = s + wg * P;
-    const int i0 = blockIdx.x * wg, ti = threadIdx.x;
-    float acc = x1_0[i0 + ti];
-    // wg a multiple of T (every instance of real.instance_set): thread ti
-    // copies column ti % T of rows ti / T, ti / T + wg / T, ... -- the same
-    // elements as the generic walk, without a division per element
-    const bool even = wg % T == 0;
-    const int r0 = ti / T, c0 = ti - r0 * T, rstep = wg / T;
-    for (int j0 = 0; j0 < n; j0 += T) {
-        if (even) {
-            for (int r = r0; r < wg; r += rstep) sA[r * P + c0] = A[(size_t)(i0 + r) * n + j0 + c0];
-        } else {
-            for (int e = ti; e < wg * T; e += wg) {
-                const int r = e / T, cc = e - r * T;
-                sA[r * P + cc] = A[(size_t)(i0 + r) * n + j0 + cc];
-            }
+// ---- TMA ring helpers (the optimized MVT kernels)
+struct alignas(64) RealTmap {
+    unsigned long long opaque[16];
+};
+__device__ __forceinline__ unsigned rk_smem(const void *p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void rk_bar_init(unsigned long long *b, unsigned c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(rk_smem(b)), "r"(c));
+}
+__device__ __forceinline__ void rk_expect(unsigned long long *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(rk_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void rk_arrive(unsigned long long *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rk_smem(b)) : "memory");
+}
+__device__ __forceinline__ void rk_wait(unsigned long long *b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "RK_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra RK_DONE;\n\t"
+        "bra RK_WAIT;\n"
+        "RK_DONE:\n\t}" ::"r"(rk_smem(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void rk_tma2d(void *dst, const RealTmap *m, unsigned long long *bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            rk_smem(dst)),
+        "l"(reinterpret_cast<unsigned long long>(m)), "r"(rk_smem(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+constexpr int kMvtMaxStages = 16;
+
+// Ring of S stages, each one j-tile of T columns (kernel 1) or rows
+// (kernel 2) for the CTA's wg outputs, behind full/empty mbarriers; thread 0
+// issues the TMA loads and refills a stage once every warp released it.
+// Kernel 1's box rows are 64/128 bytes wide and TMA-swizzled (64B/128B
+// modes) so that a quarter-warp's 128-bit reads of 8 rows hit 8 distinct
+// bank groups; kernel 2's rows are read one float per lane, consecutive.
+template <int T>
+__global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y1,
+                                                  const float *__restrict__ x1_0, float *__restrict__ x1, int n,
+                                                  int S) {
+    extern __shared__ unsigned char rk_raw[];
+    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
+    float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 1023) & ~uintptr_t(1023));
+    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int i0 = blockIdx.x * wg, steps = n / T, sf = wg * T;
+    const int boxes = (wg + 255) / 256, brows = wg < 256 ? wg : 256;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            rk_bar_init(&full[s], 1);
+            rk_bar_init(&empty[s], wg / 32);
         }
-        for (int e = ti; e < T; e += wg) sy[e] = y1[j0 + e];
-        __syncthreads();
-        for (int jj = 0; jj < T; ++jj) acc = __fmaf_rn(sA[ti * P + jj], sy[jj], acc);
-        __syncthreads();
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    x1[i0 + ti] = acc;
+    __syncthreads();
+    auto issue = [&](int slot, int step) {
+        rk_expect(&full[slot], (unsigned)(sf * 4));
+        for (int b = 0; b < boxes; ++b) rk_tma2d(st + slot * sf + b * 256 * T, &tm, &full[slot], step * T, i0 + b * brows);
+    };
+    if (tid == 0)
+        for (int s = 0; s < S && s < steps; ++s) issue(s, s);
+    const int swz = T == 32 ? (tid & 7) : ((tid >> 1) & 3);
+    float acc = x1_0[i0 + tid];
+    int slot = 0;
+    unsigned phase = 0;
+    for (int step = 0; step < steps; ++step) {
+        rk_wait(&full[slot], phase);
+        const float *row = st + slot * sf + tid * T;
+        const float4 *y4 = reinterpret_cast<const float4 *>(y1 + step * T);
+#pragma unroll
+        for (int c = 0; c < T / 4; ++c) {
+            const float4 a = *reinterpret_cast<const float4 *>(row + ((c ^ swz) << 2));
+            const float4 y = __ldg(y4 + c);
+            acc = __fmaf_rn(a.x, y.x, acc);
+            acc = __fmaf_rn(a.y, y.y, acc);
+            acc = __fmaf_rn(a.z, y.z, acc);
+            acc = __fmaf_rn(a.w, y.w, acc);
+        }
+        __syncwarp();
+        if (lane == 0) rk_arrive(&empty[slot]);
+        if (tid == 0 && step + S < steps) {
+            rk_wait(&empty[slot], phase);
+            issue(slot, step + S);
+        }
+        if (++slot == S) {
+            slot = 0;
+            phase ^= 1;
+        }
+    }
+    x1[i0 + tid] = acc;
 }
 
-// optimized kernel 2: A is already read coalesced; T entries of y2 staged per step
-__global__ void k_mvt2_opt(const float *__restrict__ A, const float *__restrict__ y2, const float *__restrict__ x2_0,
-                           float *__restrict__ x2, int n, int T) {
-    extern __shared__ float sy[];  // [T]
-    const int wg = blockDim.x;
-    const int i = blockIdx.x * wg + threadIdx.x;
-    float acc = x2_0[i];
-    for (int j0 = 0; j0 < n; j0 += T) {
-        for (int e = threadIdx.x; e < T; e += wg) sy[e] = y2[j0 + e];
-        __syncthreads();
-        for (int jj = 0; jj < T; ++jj) acc = __fmaf_rn(A[(size_t)(j0 + jj) * n + i], sy[jj], acc);
-        __syncthreads();
+__global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y2,
+                                                  const float *__restrict__ x2_0, float *__restrict__ x2, int n, int T,
+                                                  int S) {
+    extern __shared__ unsigned char rk_raw[];
+    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
+    float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
+    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int i0 = blockIdx.x * wg, steps = n / T, sf = wg * T;
+    const int boxes = (wg + 255) / 256, bcols = wg < 256 ? wg : 256;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            rk_bar_init(&full[s], 1);
+            rk_bar_init(&empty[s], wg / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    x2[i] = acc;
+    __syncthreads();
+    auto issue = [&](int slot, int step) {
+        rk_expect(&full[slot], (unsigned)(sf * 4));
+        for (int b = 0; b < boxes; ++b)
+            rk_tma2d(st + slot * sf + b * T * bcols, &tm, &full[slot], i0 + b * bcols, step * T);
+    };
+    if (tid == 0)
+        for (int s = 0; s < S && s < steps; ++s) issue(s, s);
+    const int b = tid / bcols, c = tid - b * bcols;
+    float acc = x2_0[i0 + tid];
+    int slot = 0;
+    unsigned phase = 0;
+    for (int step = 0; step < steps; ++step) {
+        rk_wait(&full[slot], phase);
+        const float *col = st + slot * sf + b * T * bcols + c;
+        const float *y = y2 + step * T;
+        for (int jj = 0; jj < T; jj += 4) {
+            const float4 yv = __ldg(reinterpret_cast<const float4 *>(y + jj));
+            acc = __fmaf_rn(col[(jj + 0) * bcols], yv.x, acc);
+            acc = __fmaf_rn(col[(jj + 1) * bcols], yv.y, acc);
+            acc = __fmaf_rn(col[(jj + 2) * bcols], yv.z, acc);
+            acc = __fmaf_rn(col[(jj + 3) * bcols], yv.w, acc);
+        }
+        __syncwarp();
+        if (lane == 0) rk_arrive(&empty[slot]);
+        if (tid == 0 && step + S < steps) {
+            rk_wait(&empty[slot], phase);
+            issue(slot, step + S);
+        }
+        if (++slot == S) {
+            slot = 0;
+            phase ^= 1;
+        }
+    }
+    x2[i0 + tid] = acc;
 }
 
 }  // namespace lmt
