@@ -276,6 +276,13 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
 int lmt_kernel_source(const lmt_instance *inst, const lmt_device *dev, int variant, int32_t flags, char *buf,
                       int64_t cap, int64_t *len_out);
 
+/* The launch plan of an instance as the measurement engine would build it on
+ * a 148-SM B200 (no GPU needed): out16 = baseline U, D, min CTAs/SM, max
+ * threads, 128-bit shifted copies; optimized U, D, min CTAs/SM, max threads,
+ * group stages, dynamic shared memory bytes, bytes per staged region, floats
+ * per region slot, feasible, CTAs, shared-region groups. */
+int lmt_plan_info(const lmt_instance *inst, const lmt_device *dev, int32_t flags, int64_t *out16);
+
 /* Kernels compiled by NVRTC so far in this process (disk-cache hits are not
  * compiles) and the host seconds spent compiling. */
 int lmt_jit_stats(int64_t *kernels_compiled, double *compile_seconds);

@@ -571,6 +571,7 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
         bd = 1;
         bu = (int)std::min<int64_t>(4, std::max<int64_t>(1, nit));
         while (bu & (bu - 1)) bu &= bu - 1;
+        while (bu > 1 && rps(bu) * stage_bytes > smem_cap) bu >>= 1;  // one group's regions must fit
         int64_t G = std::min<int64_t>(4, ngroups(bu));
         while (G > 1 && G * rps(bu) * stage_bytes > smem_cap) G--;
         const int64_t res = std::min<int64_t>({64 / std::max<int64_t>(1, warps), 32,
@@ -608,6 +609,8 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
         }
     } else {
         bd = std::min(2, dmax);  // shared-memory loads: one step of lookahead covers them
+        bu = 1;  // when no shape fits (the region alone exceeds shared memory) the variant is infeasible
+        bs = 1;
         double best = -1.0;
         for (int U : {8, 4, 2, 1}) {
             if (U > nit) continue;
@@ -1962,6 +1965,23 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
     std::copy(t.left.begin(), t.left.end(), left);
     std::copy(t.right.begin(), t.right.end(), right);
     std::copy(t.value.begin(), t.value.end(), value);
+    return LMT_OK;
+}
+
+int lmt_plan_info(const lmt_instance *inst, const lmt_device *dev, int32_t flags, int64_t *out16) {
+    if (!inst || !out16) return fail(LMT_ERR_ARG, "bad plan_info arguments");
+    if (!violations(*inst).empty()) return fail(LMT_ERR_INVALID_INSTANCE, "invalid instance");
+    const lmt_device d = dev_or_default(dev);
+    lmt_geometry g0;
+    int rc = compute_geometry(*inst, d, &g0);
+    if (rc) return rc;
+    Plan pl;
+    rc = make_plan(*inst, d, round_up(g0.alloc_w, 4), flags, nullptr, &pl);
+    if (rc) return rc;
+    const int64_t v[16] = {pl.kb.U, pl.kb.D, pl.kb.minb, pl.kb.maxt, pl.kb.vec, pl.ko.U, pl.ko.D, pl.ko.minb,
+                           pl.ko.maxt, pl.A.nstages, (int64_t)pl.dyn_smem, (int64_t)pl.A.stage_bytes,
+                           (int64_t)pl.A.stage_floats, pl.feasible ? 1 : 0, pl.ctas, pl.ko.share};
+    memcpy(out16, v, sizeof v);
     return LMT_OK;
 }
 

@@ -60,7 +60,7 @@ def rank_share(table, world: int, rank: int, sample: int = 0, seed: int = 0, fam
     if family != "all":
         rows = sweep.family_rows(table, sweep.DLA_FAMILY if family == "dla" else sweep.GRID_FAMILY)
     if sample and sample < len(rows):
-        rows = np.sort(np.random.default_rng(seed ^ 0x5A3B1E).choice(len(rows), size=sample, replace=False))
+        rows = np.sort(np.random.default_rng(seed ^ 0x5A3B1E).choice(rows, size=sample, replace=False))
     if world == 1:
         return rows
     cost = sweep.launch_cost(table.records(rows))

@@ -253,3 +253,25 @@ def test_train_matches_reference(lmtune_ref, tmp_path):
         ref_forest.save(ref, tmp_path / "r.txt")
         L.save(ours, tmp_path / "o.txt")
         assert (tmp_path / "r.txt").read_bytes() == (tmp_path / "o.txt").read_bytes()
+
+
+def test_launch_plans_fit_the_device():
+    """Every launch plan of a sweep sample (lmt_plan_info, no GPU): the
+    optimized variant's ring fits shared memory whenever it can run, work
+    units per thread stay within the kernels' limits."""
+    import ctypes
+
+    from paper_1412_6986_b200._lib import CInstance, lib
+
+    t = L.select_instance_table(L.SamplingSpec(max_instances=1_000_000, seed=0))
+    rows = np.random.default_rng(5).choice(len(t), size=3000, replace=False)
+    out = (ctypes.c_int64 * 16)()
+    cap = 227 * 1024
+    for flags in (0x8, 0x18):
+        for r in t.records(rows):
+            ci = CInstance(*[int(v) for v in r[:19]])
+            assert lib().lmt_plan_info(ctypes.byref(ci), None, flags, out) == 0
+            v = list(out)
+            assert 1 <= v[0] <= 16 and 1 <= v[1] <= 3 and 1 <= v[5] <= 8 and 1 <= v[9] <= 16, (r.tolist(), v)
+            if v[12] * 4 <= cap:  # one region fits: the ring must too
+                assert v[10] <= cap, (r.tolist(), v)
