@@ -344,7 +344,9 @@ int get_ctx(DevCtx **out) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_tma<32>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma),
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma<16>),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma<32>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_rows_opt),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
@@ -1675,7 +1677,9 @@ std::string real_violations(const lmt_real_instance &r) {
     if (wx < 1 || wy < 1 || wx * wy > 1024) { snprintf(b, sizeof b, "workgroup %lldx%lld", (long long)wx, (long long)wy); return b; }
     switch (r.kernel) {
         case 0:
-            if (T != wx || T > 32 || T % wy || n % T) return "transpose needs tile == wg_x <= 32, wg_y | tile, tile | n";
+            if (T > 64 || T % wx || (T / wx != 1 && T / wx != 2 && T / wx != 4) || T % wy || n % T)
+                return "transpose needs tile <= 64, tile / wg_x in {1, 2, 4} (columns per thread), wg_y | tile, "
+                       "tile | n";
             return "";
         case 1:
             if (T != wx || T > 32 || T % wy || n % T) return "matrixMul needs tile == wg_x <= 32, wg_y | tile, tile | n";
@@ -1717,8 +1721,17 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
     switch (r.kernel) {
         case 0: {
             const dim3 grd(n / T, n / T);
-            if (variant == 0) k_transpose_base<<<grd, blk, 0, s>>>(in[0], out, n, T);
-            else k_transpose_opt<<<grd, blk, (size_t)T * (T + 1) * 4, s>>>(in[0], out, n, T);
+            const int C = T / wx;
+            const size_t sm = (size_t)T * (T + 1) * 4;
+            if (variant == 0) {
+                if (C == 1) k_transpose_base<1><<<grd, blk, 0, s>>>(in[0], out, n, T);
+                else if (C == 2) k_transpose_base<2><<<grd, blk, 0, s>>>(in[0], out, n, T);
+                else k_transpose_base<4><<<grd, blk, 0, s>>>(in[0], out, n, T);
+            } else {
+                if (C == 1) k_transpose_opt<1><<<grd, blk, sm, s>>>(in[0], out, n, T);
+                else if (C == 2) k_transpose_opt<2><<<grd, blk, sm, s>>>(in[0], out, n, T);
+                else k_transpose_opt<4><<<grd, blk, sm, s>>>(in[0], out, n, T);
+            }
             break;
         }
         case 1: {
@@ -1776,7 +1789,8 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                 if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S * stage + 1024, s>>>(t1, in[1], in[3], out, n, S);
                 else k_mvt1_tma<16><<<grd, wx, (size_t)S * stage + 1024, s>>>(t1, in[1], in[3], out, n, S);
                 CUDA_TRY(cudaGetLastError());
-                k_mvt2_tma<<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, T, S);
+                if (T == 32) k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, S);
+                else k_mvt2_tma<16><<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, S);
             }
             break;
         }

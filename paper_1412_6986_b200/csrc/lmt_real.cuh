@@ -25,25 +25,64 @@ struct RealConv {
 };
 
 // ------------------------------------------------------------ transpose
-// B[x][y] = A[y][x], n x n. CTA = one T x T tile, blockDim (T, wy); each
-// thread walks T / wy rows of the tile (SDK transposeNaive / transposeCoalesced).
+// B[x][y] = A[y][x], n x n. CTA = one T x T tile, blockDim (T / C, wy): each
+// thread owns C adjacent columns of the tile (C-wide vector loads and
+// stores, C = T / wg_x in {1, 2, 4}) and walks T / wy rows
+// (SDK transposeNaive / transposeCoalesced; C > 1 puts more bytes in flight
+// per thread: measured on B200, tools/probes/transpose_probe.cu, a 64 x 64
+// tile with 2 columns per thread reaches 0.8 of the copy bandwidth where the
+// 32 x 32 one-column form stops at 0.55).
+template <int C>
+struct VecOf;
+template <>
+struct VecOf<1> { using T = float; };
+template <>
+struct VecOf<2> { using T = float2; };
+template <>
+struct VecOf<4> { using T = float4; };
+template <int C>
+__device__ __forceinline__ float vget(const typename VecOf<C>::T &v, int q) {
+    if constexpr (C == 1) return v;
+    else if constexpr (C == 2) return q == 0 ? v.x : v.y;
+    else return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+template <int C>
+__device__ __forceinline__ void vset(typename VecOf<C>::T &v, int q, float x) {
+    if constexpr (C == 1) v = x;
+    else if constexpr (C == 2) (q == 0 ? v.x : v.y) = x;
+    else (q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w) = x;
+}
+
+template <int C>
 __global__ void k_transpose_base(const float *__restrict__ A, float *__restrict__ B, int n, int T) {
-    const int x = blockIdx.x * T + threadIdx.x;
+    using V = typename VecOf<C>::T;
+    const int x = blockIdx.x * T + C * threadIdx.x;
     for (int j = threadIdx.y; j < T; j += blockDim.y) {
         const int y = blockIdx.y * T + j;
-        B[(size_t)x * n + y] = A[(size_t)y * n + x];  // coalesced read, strided write
+        const V v = *reinterpret_cast<const V *>(A + (size_t)y * n + x);  // coalesced read
+#pragma unroll
+        for (int q = 0; q < C; ++q) B[(size_t)(x + q) * n + y] = vget<C>(v, q);  // strided writes
     }
 }
 
+template <int C>
 __global__ void k_transpose_opt(const float *__restrict__ A, float *__restrict__ B, int n, int T) {
-    extern __shared__ float tile[];  // [T][T + 1]: the +1 makes column reads bank-conflict free
+    using V = typename VecOf<C>::T;
+    extern __shared__ float tile[];  // [T][T + 1]: the +1 keeps the column reads (nearly) bank-conflict free
     const int P = T + 1;
-    const int tx = threadIdx.x;
-    for (int j = threadIdx.y; j < T; j += blockDim.y)
-        tile[j * P + tx] = A[(size_t)(blockIdx.y * T + j) * n + blockIdx.x * T + tx];
+    const int cx = C * threadIdx.x;
+    for (int j = threadIdx.y; j < T; j += blockDim.y) {
+        const V v = *reinterpret_cast<const V *>(A + (size_t)(blockIdx.y * T + j) * n + blockIdx.x * T + cx);
+#pragma unroll
+        for (int q = 0; q < C; ++q) tile[j * P + cx + q] = vget<C>(v, q);
+    }
     __syncthreads();
-    for (int j = threadIdx.y; j < T; j += blockDim.y)
-        B[(size_t)(blockIdx.x * T + j) * n + blockIdx.y * T + tx] = tile[tx * P + j];  // coalesced write
+    for (int j = threadIdx.y; j < T; j += blockDim.y) {
+        V v;
+#pragma unroll
+        for (int q = 0; q < C; ++q) vset<C>(v, q, tile[(cx + q) * P + j]);
+        *reinterpret_cast<V *>(B + (size_t)(blockIdx.x * T + j) * n + blockIdx.y * T + cx) = v;  // coalesced write
+    }
 }
 
 // ------------------------------------------------------------ matrixMul
@@ -290,6 +329,16 @@ __device__ __forceinline__ void rk_tma2d(void *dst, const RealTmap *m, unsigned 
         "l"(reinterpret_cast<unsigned long long>(m)), "r"(rk_smem(bar)), "r"(x), "r"(y)
         : "memory");
 }
+__device__ __forceinline__ float4 rk_lds4(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float rk_lds(unsigned a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
 constexpr int kMvtMaxStages = 16;
 
 // Ring of S stages, each one j-tile of T columns (kernel 1) or rows
@@ -324,20 +373,40 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
     const int swz = T == 32 ? (tid & 7) : ((tid >> 1) & 3);
     float acc = x1_0[i0 + tid];
+    // The chain is one serial FMA per element, so the next stage's row
+    // segment and y values are loaded into registers while this stage's
+    // FMAs run (one warp per SM carries 32 chains: latency is the limit).
+    const unsigned base = rk_smem(st) + (unsigned)(tid * T * 4);
+    const float4 *y4 = reinterpret_cast<const float4 *>(y1);
+    float4 ca[T / 4], cy[T / 4], na[T / 4], ny[T / 4];
+    auto load = [&](float4 (&a)[T / 4], float4 (&y)[T / 4], int slot, int step) {
+#pragma unroll
+        for (int c = 0; c < T / 4; ++c) {
+            a[c] = rk_lds4(base + (unsigned)(slot * sf * 4) + (unsigned)(((c ^ swz) << 4)));
+            y[c] = __ldg(y4 + step * (T / 4) + c);
+        }
+    };
+    rk_wait(&full[0], 0);
+    load(ca, cy, 0, 0);
     int slot = 0;
     unsigned phase = 0;
     for (int step = 0; step < steps; ++step) {
-        rk_wait(&full[slot], phase);
-        const float *row = st + slot * sf + tid * T;
-        const float4 *y4 = reinterpret_cast<const float4 *>(y1 + step * T);
+        int ns = slot + 1;
+        unsigned nph = phase;
+        if (ns == S) {
+            ns = 0;
+            nph ^= 1;
+        }
+        if (step + 1 < steps) {
+            rk_wait(&full[ns], nph);
+            load(na, ny, ns, step + 1);
+        }
 #pragma unroll
         for (int c = 0; c < T / 4; ++c) {
-            const float4 a = *reinterpret_cast<const float4 *>(row + ((c ^ swz) << 2));
-            const float4 y = __ldg(y4 + c);
-            acc = __fmaf_rn(a.x, y.x, acc);
-            acc = __fmaf_rn(a.y, y.y, acc);
-            acc = __fmaf_rn(a.z, y.z, acc);
-            acc = __fmaf_rn(a.w, y.w, acc);
+            acc = __fmaf_rn(ca[c].x, cy[c].x, acc);
+            acc = __fmaf_rn(ca[c].y, cy[c].y, acc);
+            acc = __fmaf_rn(ca[c].z, cy[c].z, acc);
+            acc = __fmaf_rn(ca[c].w, cy[c].w, acc);
         }
         __syncwarp();
         if (lane == 0) rk_arrive(&empty[slot]);
@@ -345,16 +414,20 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
             rk_wait(&empty[slot], phase);
             issue(slot, step + S);
         }
-        if (++slot == S) {
-            slot = 0;
-            phase ^= 1;
+#pragma unroll
+        for (int c = 0; c < T / 4; ++c) {
+            ca[c] = na[c];
+            cy[c] = ny[c];
         }
+        slot = ns;
+        phase = nph;
     }
     x1[i0 + tid] = acc;
 }
 
+template <int T>
 __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y2,
-                                                  const float *__restrict__ x2_0, float *__restrict__ x2, int n, int T,
+                                                  const float *__restrict__ x2_0, float *__restrict__ x2, int n,
                                                   int S) {
     extern __shared__ unsigned char rk_raw[];
     __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
@@ -379,18 +452,37 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
     const int b = tid / bcols, c = tid - b * bcols;
     float acc = x2_0[i0 + tid];
+    const unsigned base = rk_smem(st) + (unsigned)((b * T * bcols + c) * 4);
+    const float4 *y4 = reinterpret_cast<const float4 *>(y2);
+    float ca[T], na[T];
+    float4 cy[T / 4], ny[T / 4];
+    auto load = [&](float (&a)[T], float4 (&y)[T / 4], int slot, int step) {
+#pragma unroll
+        for (int jj = 0; jj < T; ++jj) a[jj] = rk_lds(base + (unsigned)((slot * sf + jj * bcols) * 4));
+#pragma unroll
+        for (int q = 0; q < T / 4; ++q) y[q] = __ldg(y4 + step * (T / 4) + q);
+    };
+    rk_wait(&full[0], 0);
+    load(ca, cy, 0, 0);
     int slot = 0;
     unsigned phase = 0;
     for (int step = 0; step < steps; ++step) {
-        rk_wait(&full[slot], phase);
-        const float *col = st + slot * sf + b * T * bcols + c;
-        const float *y = y2 + step * T;
-        for (int jj = 0; jj < T; jj += 4) {
-            const float4 yv = __ldg(reinterpret_cast<const float4 *>(y + jj));
-            acc = __fmaf_rn(col[(jj + 0) * bcols], yv.x, acc);
-            acc = __fmaf_rn(col[(jj + 1) * bcols], yv.y, acc);
-            acc = __fmaf_rn(col[(jj + 2) * bcols], yv.z, acc);
-            acc = __fmaf_rn(col[(jj + 3) * bcols], yv.w, acc);
+        int ns = slot + 1;
+        unsigned nph = phase;
+        if (ns == S) {
+            ns = 0;
+            nph ^= 1;
+        }
+        if (step + 1 < steps) {
+            rk_wait(&full[ns], nph);
+            load(na, ny, ns, step + 1);
+        }
+#pragma unroll
+        for (int q = 0; q < T / 4; ++q) {
+            acc = __fmaf_rn(ca[4 * q + 0], cy[q].x, acc);
+            acc = __fmaf_rn(ca[4 * q + 1], cy[q].y, acc);
+            acc = __fmaf_rn(ca[4 * q + 2], cy[q].z, acc);
+            acc = __fmaf_rn(ca[4 * q + 3], cy[q].w, acc);
         }
         __syncwarp();
         if (lane == 0) rk_arrive(&empty[slot]);
@@ -398,10 +490,12 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
             rk_wait(&empty[slot], phase);
             issue(slot, step + S);
         }
-        if (++slot == S) {
-            slot = 0;
-            phase ^= 1;
-        }
+#pragma unroll
+        for (int jj = 0; jj < T; ++jj) ca[jj] = na[jj];
+#pragma unroll
+        for (int q = 0; q < T / 4; ++q) cy[q] = ny[q];
+        slot = ns;
+        phase = nph;
     }
     x2[i0 + tid] = acc;
 }

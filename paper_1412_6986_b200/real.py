@@ -28,7 +28,8 @@ class RealInstance:
     n: int           # square problem size
     wg_x: int
     wg_y: int
-    tile: int = 0    # transpose / matrixMul tile (== wg_x), MVT j-tile, convolution outputs per thread
+    tile: int = 0    # transpose tile (wg_x * columns per thread) / matrixMul tile (== wg_x), MVT j-tile,
+    #                  convolution outputs per thread
     radius: int = 0  # convolution radius
 
     @property
@@ -46,16 +47,18 @@ def validate(inst: RealInstance) -> str:
 
 
 def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 2048, n_mvt: int = 4096) -> list:
-    """The configs[1] instance set: 15 transpose (tile T in {8,16,32} x rows
-    per CTA step), 14 matrixMul (T in {4..32} x outputs per thread), 24
+    """The configs[1] instance set: 18 transpose (tile T in {8,16,32} x rows
+    per CTA step, and 64 x 64 tiles with two columns per thread), 14 matrixMul (T in {4..32} x outputs per thread), 24
     convolution (radius in {1,2,4,8} x 6 workgroups), 10 MVT (workgroup x
-    j-tile), plus 5 transpose and 8 convolution instances at 8192 x 8192
+    j-tile), plus 7 transpose and 8 convolution instances at 8192 x 8192
     (arrays well beyond L2) for the HBM roof."""
     out = []
     for T in (8, 16, 32):
         for wy in (1, 2, 4, 8, 16, 32):
             if wy <= T:
                 out.append(RealInstance(0, n_transpose, T, wy, tile=T))
+    for wy in (4, 8, 16):  # 64 x 64 tiles, two columns per thread
+        out.append(RealInstance(0, n_transpose, 32, wy, tile=64))
     for T in (4, 8, 16, 32):
         for W in (1, 2, 4, 8):
             if W <= T and T // W >= 1 and W in (1, 2, 4) + ((8,) if T >= 16 else ()):
@@ -70,6 +73,8 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
     for wy in (1, 2, 4, 8):  # 32 .. 4 elements per thread in flight
         out.append(RealInstance(0, 8192, 32, wy, tile=32))
     out.append(RealInstance(0, 8192, 16, 16, tile=16))
+    for wy in (4, 8):
+        out.append(RealInstance(0, 8192, 32, wy, tile=64))
     for R in (1, 2, 4, 8):
         for W in (1, 4):  # outputs per thread
             out.append(RealInstance(2, 8192, 32, 8, tile=W, radius=R))
