@@ -1768,7 +1768,13 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                 // 64/128-byte rows) and [T][wg] (kernel 2) tiles by TMA
                 const int64_t stage = (int64_t)wx * T * 4, cap = smem_optin - 2048;
                 const int S = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage, (int64_t)n / T});
-                if (S < 1) return fail(LMT_ERR_TOO_LARGE, "MVT tile needs %lld bytes of shared memory", (long long)stage);
+                // kernel 1: stages of up to 256 columns (KB boxes of T), two of them at least when they fit
+                int KB = kMvtStageCols / T;
+                while (KB > 1 && ((int64_t)wx * KB * T * 4 * 2 > cap || n % (KB * T))) KB >>= 1;
+                const int64_t stage1 = (int64_t)wx * KB * T * 4;
+                const int S1 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage1, (int64_t)n / (KB * T)});
+                if (S < 1 || S1 < 1)
+                    return fail(LMT_ERR_TOO_LARGE, "MVT stages need %lld bytes of shared memory", (long long)stage1);
                 CUtensorMap m1, m2;
                 const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
                 const cuuint64_t strides[1] = {(cuuint64_t)n * 4};
@@ -1786,8 +1792,8 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                     return fail(LMT_ERR_CUDA, "MVT tensor maps: %d %d", (int)e1, (int)e2);
                 const RealTmap t1 = *reinterpret_cast<const RealTmap *>(&m1);
                 const RealTmap t2 = *reinterpret_cast<const RealTmap *>(&m2);
-                if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S * stage + 1024, s>>>(t1, in[1], in[3], out, n, S);
-                else k_mvt1_tma<16><<<grd, wx, (size_t)S * stage + 1024, s>>>(t1, in[1], in[3], out, n, S);
+                if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 1024, s>>>(t1, in[1], in[3], out, n, S1, KB);
+                else k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 1024, s>>>(t1, in[1], in[3], out, n, S1, KB);
                 CUDA_TRY(cudaGetLastError());
                 if (T == 32) k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, S);
                 else k_mvt2_tma<16><<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, S);

@@ -341,21 +341,26 @@ __device__ __forceinline__ float rk_lds(unsigned a) {
 }
 constexpr int kMvtMaxStages = 16;
 
-// Ring of S stages, each one j-tile of T columns (kernel 1) or rows
-// (kernel 2) for the CTA's wg outputs, behind full/empty mbarriers; thread 0
-// issues the TMA loads and refills a stage once every warp released it.
-// Kernel 1's box rows are 64/128 bytes wide and TMA-swizzled (64B/128B
-// modes) so that a quarter-warp's 128-bit reads of 8 rows hit 8 distinct
-// bank groups; kernel 2's rows are read one float per lane, consecutive.
+// Kernel 1: a ring of S stages, each 256 columns of the CTA's wg rows as
+// 256 / T boxes of T columns (1 KB of every row per stage, so DRAM sees
+// row segments of 1 KB rather than 128 B); the boxes' 64/128-byte rows are
+// TMA-swizzled (64B/128B modes) so that a quarter-warp's 128-bit reads of 8
+// rows hit 8 distinct bank groups. Kernel 2: stages of T rows x wg columns,
+// read one float per lane (consecutive). Thread 0 issues the TMA loads and
+// refills a stage once every warp released it; each thread's registers hold
+// the next box (kernel 1) / stage (kernel 2) while the current one's FMAs
+// run -- one warp per SM carries the serial chains, so latency is the limit.
+constexpr int kMvtStageCols = 256;
 template <int T>
 __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y1,
                                                   const float *__restrict__ x1_0, float *__restrict__ x1, int n,
-                                                  int S) {
+                                                  int S, int KB) {
+    // KB boxes of T columns per stage (kMvtStageCols columns, fewer for wide workgroups)
     extern __shared__ unsigned char rk_raw[];
     __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
     float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 1023) & ~uintptr_t(1023));
     const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
-    const int i0 = blockIdx.x * wg, steps = n / T, sf = wg * T;
+    const int i0 = blockIdx.x * wg, steps = n / (KB * T), sf = wg * KB * T;
     const int boxes = (wg + 255) / 256, brows = wg < 256 ? wg : 256;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -367,39 +372,43 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
     __syncthreads();
     auto issue = [&](int slot, int step) {
         rk_expect(&full[slot], (unsigned)(sf * 4));
-        for (int b = 0; b < boxes; ++b) rk_tma2d(st + slot * sf + b * 256 * T, &tm, &full[slot], step * T, i0 + b * brows);
+        for (int kb = 0; kb < KB; ++kb)
+            for (int b = 0; b < boxes; ++b)
+                rk_tma2d(st + slot * sf + kb * wg * T + b * 256 * T, &tm, &full[slot], (step * KB + kb) * T,
+                         i0 + b * brows);
     };
     if (tid == 0)
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
     const int swz = T == 32 ? (tid & 7) : ((tid >> 1) & 3);
     float acc = x1_0[i0 + tid];
-    // The chain is one serial FMA per element, so the next stage's row
-    // segment and y values are loaded into registers while this stage's
-    // FMAs run (one warp per SM carries 32 chains: latency is the limit).
     const unsigned base = rk_smem(st) + (unsigned)(tid * T * 4);
     const float4 *y4 = reinterpret_cast<const float4 *>(y1);
     float4 ca[T / 4], cy[T / 4], na[T / 4], ny[T / 4];
-    auto load = [&](float4 (&a)[T / 4], float4 (&y)[T / 4], int slot, int step) {
+    // sub-step k = (stage k / KB, box kb = k % KB): its T columns are j = k * T ..
+    auto load = [&](float4 (&a)[T / 4], float4 (&y)[T / 4], int slot, int kb, int k) {
+        const unsigned bx = base + (unsigned)((slot * sf + kb * wg * T) * 4);
 #pragma unroll
         for (int c = 0; c < T / 4; ++c) {
-            a[c] = rk_lds4(base + (unsigned)(slot * sf * 4) + (unsigned)(((c ^ swz) << 4)));
-            y[c] = __ldg(y4 + step * (T / 4) + c);
+            a[c] = rk_lds4(bx + (unsigned)((c ^ swz) << 4));
+            y[c] = __ldg(y4 + k * (T / 4) + c);
         }
     };
+    const int total = steps * KB;
     rk_wait(&full[0], 0);
-    load(ca, cy, 0, 0);
-    int slot = 0;
+    load(ca, cy, 0, 0, 0);
+    int slot = 0, kb = 0, step = 0;
     unsigned phase = 0;
-    for (int step = 0; step < steps; ++step) {
-        int ns = slot + 1;
+    for (int k = 0; k < total; ++k) {
+        const bool last = kb == KB - 1;  // the stage's last box
+        int ns = slot;
         unsigned nph = phase;
-        if (ns == S) {
+        if (last && ++ns == S) {
             ns = 0;
             nph ^= 1;
         }
-        if (step + 1 < steps) {
-            rk_wait(&full[ns], nph);
-            load(na, ny, ns, step + 1);
+        if (k + 1 < total) {
+            if (last) rk_wait(&full[ns], nph);
+            load(na, ny, ns, last ? 0 : kb + 1, k + 1);
         }
 #pragma unroll
         for (int c = 0; c < T / 4; ++c) {
@@ -408,11 +417,17 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
             acc = __fmaf_rn(ca[c].z, cy[c].z, acc);
             acc = __fmaf_rn(ca[c].w, cy[c].w, acc);
         }
-        __syncwarp();
-        if (lane == 0) rk_arrive(&empty[slot]);
-        if (tid == 0 && step + S < steps) {
-            rk_wait(&empty[slot], phase);
-            issue(slot, step + S);
+        if (last) {
+            __syncwarp();
+            if (lane == 0) rk_arrive(&empty[slot]);
+            if (tid == 0 && step + S < steps) {
+                rk_wait(&empty[slot], phase);
+                issue(slot, step + S);
+            }
+            ++step;
+            kb = 0;
+        } else {
+            ++kb;
         }
 #pragma unroll
         for (int c = 0; c < T / 4; ++c) {
