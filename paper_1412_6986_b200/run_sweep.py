@@ -45,6 +45,10 @@ def _args(argv=None):
                          "GRID_FAMILY)")
     ap.add_argument("--concurrent", action="store_true",
                     help="launches of <= 74 CTAs in disjoint SM partitions (the bench's placement)")
+    ap.add_argument("--regblock", action="store_true",
+                    help="register-blocked variants (units sharing home coordinates load once) instead of the "
+                         "literal ones (DESIGN.md 5, the measurement contract)")
+    ap.add_argument("--warm-l2", action="store_true", help="no L2 flush before each whole-device variant")
     ap.add_argument("--samples", type=int, default=0,
                     help="output cells per instance read back into the chunk files (sweep.sample_cells), so an "
                          "independent checker can compare them with the CPU reference")
@@ -96,7 +100,7 @@ def run(argv=None) -> dict:
     t0 = time.time()
     rec = table.records(mine)
     fb = features_records(rec)
-    mode = dict(concurrent=args.concurrent)
+    mode = dict(concurrent=args.concurrent, regblock=args.regblock, warm_l2=args.warm_l2)
     measure.prepare_records(rec, **mode)
     t_prep = time.time() - t0
 
@@ -147,6 +151,7 @@ def run(argv=None) -> dict:
     labels = ldist.all_gather_labels(np.concatenate([lab, extra], 1), device=device, sizes=sizes)
     summary = {"rank": rank, "world": world, "max_instances": args.max_instances, "seed": args.seed,
                "family": args.family, "sample": args.sample, "concurrent": args.concurrent,
+               "regblock": args.regblock, "warm_l2": args.warm_l2,
                "rows": int(len(mine)), "chunks_resumed": resumed,
                "prepare_s": t_prep, "measure_s": t_meas,
                "instances_per_s": (len(mine) - resumed * args.chunk) / t_meas if t_meas > 0 else None,
