@@ -268,6 +268,17 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
                       int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left,
                       int32_t *right, double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used);
 
+/* forest.train's trees on the GPU (forest.py:117-163), all `ntrees` trees in
+ * one call, bit-identical to lmt_rf_train_tree / the reference: samples =
+ * [ntrees][nrows] bootstrap rows, draws = [ntrees][ndraws][k] sorted feature
+ * subsets (numpy's draws, as for lmt_rf_train_tree). Outputs [ntrees][cap]
+ * node arrays and the node count per tree. LMT_ERR_TOO_LARGE when a tree
+ * needs more draws (draws_used[t] = -1) or more than `cap` nodes (-2). */
+int lmt_rf_train_gpu(const double *X, const double *y, int64_t nrows, int32_t nfeat, int32_t ntrees,
+                     const int64_t *samples, const int32_t *draws, int64_t ndraws, int32_t k, int32_t max_depth,
+                     int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left,
+                     int32_t *right, double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used);
+
 /* The CUDA source the specialised kernel of (instance, variant) is compiled
  * from -- its #defines then the kernel text -- the counterpart of
  * codegen.emit_baseline / emit_optimized (codegen.py:336-354). flags: the

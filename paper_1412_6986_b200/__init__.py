@@ -56,6 +56,7 @@ from .forest import (
     speedup_to_target,
     train,
     train_arrays,
+    train_arrays_gpu,
 )
 from .geometry import (
     AffineAccess,

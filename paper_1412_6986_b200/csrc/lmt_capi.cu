@@ -24,6 +24,7 @@
 #include "lmt_features.cuh"
 #include "lmt_real.cuh"
 #include "lmt_train.h"
+#include "lmt_train_gpu.cuh"
 
 #ifndef LMT_VERSION
 #define LMT_VERSION "lmt_b200 0.1.0 sm_100a"
@@ -1985,6 +1986,105 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
     std::copy(t.left.begin(), t.left.end(), left);
     std::copy(t.right.begin(), t.right.end(), right);
     std::copy(t.value.begin(), t.value.end(), value);
+    return LMT_OK;
+}
+
+int lmt_rf_train_gpu(const double *X, const double *y, int64_t nrows, int32_t nfeat, int32_t ntrees,
+                     const int64_t *samples, const int32_t *draws, int64_t ndraws, int32_t k, int32_t max_depth,
+                     int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left, int32_t *right,
+                     double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used) {
+    if (!X || !y || !samples || !draws || !nodes_out || !draws_used || nrows < 1 || nfeat < 1 || ntrees < 1 ||
+        k < 1 || k > kRfMaxK || k > nfeat || ndraws < 1 || cap < 1 || min_samples_leaf < 1)
+        return fail(LMT_ERR_ARG, "bad train arguments");
+    if (nrows >= (1ll << 30) / (nfeat + 1)) return fail(LMT_ERR_TOO_LARGE, "training set too large");
+    const int64_t n = nrows, T = ntrees;
+    std::vector<int32_t> s32((size_t)(T * n));
+    for (int64_t i = 0; i < T * n; i++) {
+        if (samples[i] < 0 || samples[i] >= nrows) return fail(LMT_ERR_ARG, "sample row out of range");
+        s32[(size_t)i] = (int32_t)samples[i];
+    }
+    for (int64_t i = 0; i < T * ndraws * k; i++)
+        if (draws[i] < 0 || draws[i] >= nfeat) return fail(LMT_ERR_ARG, "feature draw out of range");
+    DevCtx *c;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int rc = get_ctx(&c);
+        if (rc) return rc;
+    }
+    cudaStream_t s = c->stream;
+    int64_t N2 = 1;
+    while (N2 < n) N2 <<= 1;
+    // device buffers, released on every path
+    std::vector<void *> bufs;
+    struct Guard {
+        std::vector<void *> *b;
+        ~Guard() {
+            for (void *p : *b) cudaFree(p);
+        }
+    } guard{&bufs};
+    auto alloc = [&](void **p, size_t bytes) -> int {
+        CUDA_TRY(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+        bufs.push_back(*p);
+        return LMT_OK;
+    };
+    RfTrainArgs A{};
+    double *dX, *dy, *keys;
+    int32_t *dsamp, *ddraws, *pos;
+    int rc = 0;
+    if ((rc = alloc((void **)&dX, sizeof(double) * n * nfeat)) || (rc = alloc((void **)&dy, sizeof(double) * n)) ||
+        (rc = alloc((void **)&dsamp, sizeof(int32_t) * T * n)) ||
+        (rc = alloc((void **)&ddraws, sizeof(int32_t) * T * ndraws * k)) ||
+        (rc = alloc((void **)&keys, sizeof(double) * T * nfeat * N2)) ||
+        (rc = alloc((void **)&pos, sizeof(int32_t) * T * nfeat * N2)) ||
+        (rc = alloc((void **)&A.sorted, sizeof(int32_t) * T * (nfeat + 1) * n)) ||
+        (rc = alloc((void **)&A.tmp, sizeof(int32_t) * T * n)) || (rc = alloc((void **)&A.flag, T * n)) ||
+        (rc = alloc((void **)&A.xs, sizeof(double) * T * k * n)) ||
+        (rc = alloc((void **)&A.ys, sizeof(double) * T * k * n)) ||
+        (rc = alloc((void **)&A.s1, sizeof(double) * T * k * n)) ||
+        (rc = alloc((void **)&A.s2, sizeof(double) * T * k * n)) ||
+        (rc = alloc((void **)&A.stack, sizeof(int32_t) * T * (n + 1) * 4)) ||
+        (rc = alloc((void **)&A.feature, sizeof(int32_t) * T * cap)) ||
+        (rc = alloc((void **)&A.left, sizeof(int32_t) * T * cap)) ||
+        (rc = alloc((void **)&A.right, sizeof(int32_t) * T * cap)) ||
+        (rc = alloc((void **)&A.threshold, sizeof(double) * T * cap)) ||
+        (rc = alloc((void **)&A.value, sizeof(double) * T * cap)) ||
+        (rc = alloc((void **)&A.nodes_out, sizeof(int64_t) * T)) ||
+        (rc = alloc((void **)&A.draws_used, sizeof(int64_t) * T)))
+        return rc;
+    CUDA_TRY(cudaMemcpyAsync(dX, X, sizeof(double) * n * nfeat, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dsamp, s32.data(), sizeof(int32_t) * T * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ddraws, draws, sizeof(int32_t) * T * ndraws * k, cudaMemcpyHostToDevice, s));
+    k_rf_presort<<<dim3((unsigned)nfeat + 1, (unsigned)T), kRfTrainThreads, 0, s>>>(dX, dsamp, (int)n, nfeat, (int)N2,
+                                                                                  keys, pos, A.sorted);
+    CUDA_TRY(cudaGetLastError());
+    A.X = dX;
+    A.y = dy;
+    A.samples = dsamp;
+    A.draws = ddraws;
+    A.n = (int)n;
+    A.nfeat = nfeat;
+    A.k = k;
+    A.ndraws = (int)ndraws;
+    A.max_depth = max_depth;
+    A.msl = min_samples_leaf;
+    A.cap = cap;
+    k_rf_build<<<(unsigned)T, kRfTrainThreads, 0, s>>>(A);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(nodes_out, A.nodes_out, sizeof(int64_t) * T, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(draws_used, A.draws_used, sizeof(int64_t) * T, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(feature, A.feature, sizeof(int32_t) * T * cap, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(threshold, A.threshold, sizeof(double) * T * cap, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(left, A.left, sizeof(int32_t) * T * cap, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(right, A.right, sizeof(int32_t) * T * cap, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(value, A.value, sizeof(double) * T * cap, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t t = 0; t < T; t++) {
+        if (draws_used[t] == -1) return fail(LMT_ERR_TOO_LARGE, "tree %lld needs more than %lld feature draws",
+                                             (long long)t, (long long)ndraws);
+        if (draws_used[t] == -2) return fail(LMT_ERR_TOO_LARGE, "tree %lld exceeds %lld nodes", (long long)t,
+                                             (long long)cap);
+    }
     return LMT_OK;
 }
 

@@ -144,6 +144,52 @@ def train_arrays(X, y, hp: Hyperparams, feature_names=None, threads: int = 1) ->
     return Forest(hyperparams=hp, feature_names=tuple(feature_names), trees=trees)
 
 
+def train_arrays_gpu(X, y, hp: Hyperparams, feature_names=None) -> Forest:
+    """train_arrays with every tree built on the GPU in one call
+    (lmt_rf_train_gpu, one CTA per tree; csrc/lmt_train_gpu.cuh), bit-identical
+    to the reference's forest.train_arrays (forest.py:166-188). The bootstrap
+    rows and per-node feature subsets are numpy's draws, made here in the
+    reference's order."""
+    from .seeding import mix_seed
+
+    X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
+    if X.ndim != 2 or len(X) != len(y):
+        raise ValueError(f"bad training shapes {X.shape} vs {y.shape}")
+    if len(y) == 0:
+        raise ValueError("empty training set")
+    if feature_names is None:
+        feature_names = tuple(f"f{i}" for i in range(X.shape[1]))
+    n, nfeat = X.shape
+    T = hp.num_trees
+    seeds = [mix_seed(hp.seed, t) for t in range(T)]
+    ndraws = min(2 * n + 1, 4096)
+    cap = 2 * n + 1
+    vp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    while True:
+        drawn = [_tree_draws(sd, n, nfeat, hp, ndraws) for sd in seeds]
+        samples = np.ascontiguousarray(np.stack([d[0] for d in drawn]), dtype=np.int64)
+        draws = np.ascontiguousarray(np.stack([d[2] for d in drawn]), dtype=np.int32)
+        k = draws.shape[2]
+        feat = np.empty((T, cap), dtype=np.int32)
+        thr = np.empty((T, cap), dtype=np.float64)
+        left = np.empty((T, cap), dtype=np.int32)
+        right = np.empty((T, cap), dtype=np.int32)
+        val = np.empty((T, cap), dtype=np.float64)
+        nodes = np.zeros(T, dtype=np.int64)
+        used = np.zeros(T, dtype=np.int64)
+        rc = lib().lmt_rf_train_gpu(vp(X), vp(y), n, nfeat, T, vp(samples), vp(draws), ndraws, k,
+                                    -1 if hp.max_depth is None else hp.max_depth, hp.min_samples_leaf, vp(feat),
+                                    vp(thr), vp(left), vp(right), vp(val), cap, vp(nodes), vp(used))
+        if rc != 0 and (used == -1).any() and ndraws < 2 * n + 1:
+            ndraws = min(2 * n + 1, ndraws * 4)  # more split attempts than drawn: draw more
+            continue
+        check(rc, what="rf_train_gpu")
+        trees = [Tree(feat[t, :m].copy(), thr[t, :m].copy(), left[t, :m].copy(), right[t, :m].copy(),
+                      val[t, :m].copy(), oob_indices=drawn[t][1]) for t, m in enumerate(nodes)]
+        return Forest(hyperparams=hp, feature_names=tuple(feature_names), trees=trees)
+
+
 def train(rows, hp: Hyperparams = Hyperparams(), threads: int = 1) -> Forest:
     """forest.train (forest.py:191-196): rows with .features and .speedup;
     target log2(speedup), infeasible floored at -10."""

@@ -259,7 +259,33 @@ def test_config4_forest_on_gpu_features_matches_reference():
     # (pre-order) forest; the model file is the canonical form
     L.save(ours, out.name + ".ours")
     with gzip.open(f"{GOLDEN_DIR}/forest_sweep100k.txt.gz", "rb") as fh:
-        assert open(out.name + ".ours", "rb").read() == fh.read()
+        golden = fh.read()
+    assert open(out.name + ".ours", "rb").read() == golden
+    # and trained on the GPU (lmt_rf_train_gpu, one CTA per tree)
+    gpu = L.train_arrays_gpu(tr.X, y, L.Hyperparams(num_trees=20, features_per_node=4, seed=0),
+                             feature_names=f.feature_names)
+    L.save(gpu, out.name + ".gpu")
+    assert open(out.name + ".gpu", "rb").read() == golden
+
+
+def test_gpu_training_matches_native_trainer():
+    """forest.train on the GPU node for node against the
+    native trainer, which tests/test_host.py pins to the reference: default
+    hyperparameters, depth / leaf-size limits, no bootstrap, many features
+    per node."""
+    ev = np.load(f"{GOLDEN_DIR}/forest_eval.npz")
+    X = ev["X"][:1500]
+    y = np.array([L.speedup_to_target(s) for s in ev["speedup"][:1500]])
+    for hp_args in (dict(num_trees=6, features_per_node=4, seed=3),
+                    dict(num_trees=3, features_per_node=6, seed=1, max_depth=7, min_samples_leaf=3),
+                    dict(num_trees=2, features_per_node=18, seed=9, bootstrap=False)):
+        hp = L.Hyperparams(**hp_args)
+        cpu = L.train_arrays(X, y, hp, threads=2)
+        gpu = L.train_arrays_gpu(X, y, hp)
+        assert len(cpu.trees) == len(gpu.trees)
+        for a, b in zip(cpu.trees, gpu.trees):
+            for fld in ("feature", "threshold", "left", "right", "value"):
+                assert np.array_equal(getattr(a, fld), getattr(b, fld)), (hp_args, fld)
 
 
 def test_run_sweep_checkpoint_resume_and_dataset(tmp_path):
