@@ -242,14 +242,24 @@ def launch_floor(records: np.ndarray, res: np.ndarray, hbm_gbs: float) -> dict:
     from .sweep import floor_seconds
 
     ch, iss = floor_seconds(records)
-    fl, t = [], []
+    fl, t, kind = [], [], []
     for col in ("t_base_ms", "t_opt_ms"):
         ran = res[col] > 0
-        fl.append(np.maximum(np.maximum(ch[ran], iss[ran]), res["alg_bytes"][ran] / (hbm_gbs * 1e9)))
+        parts = np.stack([res["alg_bytes"][ran] / (hbm_gbs * 1e9), ch[ran], iss[ran]])
+        fl.append(parts.max(0))
+        kind.append(parts.argmax(0))
         t.append(res[col][ran] / 1e3)
-    fl, t = np.concatenate(fl), np.concatenate(t)
-    return {"frac": float(fl.sum() / t.sum()) if t.sum() > 0 else 0.0, "floor_s": float(fl.sum()),
-            "kernel_s": float(t.sum())}
+    fl, t, kind = np.concatenate(fl), np.concatenate(t), np.concatenate(kind)
+    out = {"frac": float(fl.sum() / t.sum()) if t.sum() > 0 else 0.0, "floor_s": float(fl.sum()),
+           "kernel_s": float(t.sum()), "by_binding_floor": {}}
+    # which floor binds each launch: HBM bytes, the per-thread chain (few
+    # threads: the launch shape), or the per-SM fp32 issue
+    for k, name in enumerate(("hbm", "thread_chain", "sm_issue")):
+        m = kind == k
+        if m.any():
+            out["by_binding_floor"][name] = {"launches": int(m.sum()), "floor_s": float(fl[m].sum()),
+                                             "kernel_s": float(t[m].sum()), "frac": float(fl[m].sum() / t[m].sum())}
+    return out
 
 
 def roofline(res: np.ndarray, hbm_gbs: float, fp32_tflops: float) -> dict:
@@ -263,13 +273,14 @@ def roofline(res: np.ndarray, hbm_gbs: float, fp32_tflops: float) -> dict:
     kernel time against that peak, and ``frac_of_binding`` = summed per-launch
     roof time / summed measured time, i.e. how close the launches are to
     their own binding roofs."""
-    t, b, f = [], [], []
+    t, b, f, c = [], [], [], []
     for col in ("t_base_ms", "t_opt_ms"):
         ran = res[col] > 0
         t.append(res[col][ran] / 1e3)
         b.append(res["alg_bytes"][ran])
         f.append(res["alg_flops"][ran])
-    t, b, f = np.concatenate(t), np.concatenate(b), np.concatenate(f)
+        c.append(res["ctas"][ran])
+    t, b, f, c = np.concatenate(t), np.concatenate(b), np.concatenate(f), np.concatenate(c)
     if t.size == 0 or t.sum() <= 0:
         return {}
     t_hbm = b / (hbm_gbs * 1e9)
@@ -287,10 +298,17 @@ def roofline(res: np.ndarray, hbm_gbs: float, fp32_tflops: float) -> dict:
     else:
         ach = float(f.sum() / T / 1e12)
         out.update(achieved=ach, peak=fp32_tflops, unit="TFLOP/s", frac=ach / fp32_tflops)
-    if hbm_bound.any():  # the memory-bound subset on its own roof
-        tb = float(t[hbm_bound].sum())
-        out["hbm_subset"] = {"achieved": float(b[hbm_bound].sum() / tb / 1e9), "peak": hbm_gbs, "unit": "GB/s",
-                             "frac": float(b[hbm_bound].sum() / tb / 1e9 / hbm_gbs), "kernel_s": tb}
+    if hbm_bound.any():  # the memory-bound subset on its own roof, split by whether a launch can fill the chip
+        def sub(m):
+            tb = float(t[m].sum())
+            return {"launches": int(m.sum()), "achieved": float(b[m].sum() / tb / 1e9), "peak": hbm_gbs,
+                    "unit": "GB/s", "frac": float(b[m].sum() / tb / 1e9 / hbm_gbs), "kernel_s": tb}
+
+        out["hbm_subset"] = sub(hbm_bound)
+        full = c >= 2 * 148  # at least two CTAs per SM
+        for name, m in (("fills_chip", hbm_bound & full), ("cannot_fill_chip", hbm_bound & ~full)):
+            if m.any():
+                out["hbm_subset"][name] = sub(m)
     return out
 
 
