@@ -349,10 +349,12 @@ int get_ctx(DevCtx **out) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma<32>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_rows_opt),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_conv_cols_opt),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        for (const void *kf : {reinterpret_cast<const void *>(k_conv_rows_opt<0>), reinterpret_cast<const void *>(k_conv_rows_opt<1>),
+                               reinterpret_cast<const void *>(k_conv_rows_opt<2>), reinterpret_cast<const void *>(k_conv_rows_opt<4>),
+                               reinterpret_cast<const void *>(k_conv_rows_opt<8>), reinterpret_cast<const void *>(k_conv_cols_opt<0>),
+                               reinterpret_cast<const void *>(k_conv_cols_opt<1>), reinterpret_cast<const void *>(k_conv_cols_opt<2>),
+                               reinterpret_cast<const void *>(k_conv_cols_opt<4>), reinterpret_cast<const void *>(k_conv_cols_opt<8>)})
+            CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         c.device = dev;
     }
     if (!g_encode) {
@@ -1750,13 +1752,23 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
             const RealConv c = real_weights(r.radius);
             const int R = r.radius, W = T;
             const dim3 grr(n / (wx * W), n / wy), grc(n / wx, n / (wy * W));
-            if (variant == 0) {
-                k_conv_rows_base<<<grr, blk, 0, s>>>(in[0], tmp, n, R, W, c);
-                k_conv_cols_base<<<grc, blk, 0, s>>>(tmp, out, n, R, W, c);
-            } else {
-                k_conv_rows_opt<<<grr, blk, (size_t)wy * (W * wx + 2 * R) * 4, s>>>(in[0], tmp, n, R, W, c);
-                k_conv_cols_opt<<<grc, blk, (size_t)(W * wy + 2 * R) * wx * 4, s>>>(tmp, out, n, R, W, c);
+            const size_t smr = (size_t)wy * (W * wx + 2 * R) * 4, smc = (size_t)(W * wy + 2 * R) * wx * 4;
+#define LMT_CONV(RR)                                                                     \
+    if (variant == 0) {                                                                  \
+        k_conv_rows_base<RR><<<grr, blk, 0, s>>>(in[0], tmp, n, R, W, c);                \
+        k_conv_cols_base<RR><<<grc, blk, 0, s>>>(tmp, out, n, R, W, c);                  \
+    } else {                                                                             \
+        k_conv_rows_opt<RR><<<grr, blk, smr, s>>>(in[0], tmp, n, R, W, c);               \
+        k_conv_cols_opt<RR><<<grc, blk, smc, s>>>(tmp, out, n, R, W, c);                 \
+    }
+            switch (R) {
+                case 1: LMT_CONV(1) break;
+                case 2: LMT_CONV(2) break;
+                case 4: LMT_CONV(4) break;
+                case 8: LMT_CONV(8) break;
+                default: LMT_CONV(0) break;
             }
+#undef LMT_CONV
             break;
         }
         case 3: {

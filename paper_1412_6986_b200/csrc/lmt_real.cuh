@@ -170,71 +170,103 @@ __global__ void k_matmul_opt(const float *__restrict__ A, const float *__restric
 // rows: out[y][x] = sum_{k=-R..R} in[y][x+k] * w[R-k]; cols: out[y][x] = sum_k in[y+k][x] * w[R-k];
 // taps outside the image read 0. blockDim (wx, wy); each thread computes W
 // outputs, blockDim apart along the pass direction (the tiling factor: W
-// independent loads in flight per tap).
-__global__ void k_conv_rows_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+// independent chains). RR is the radius when it is a compile-time constant
+// (the instance set's 1, 2, 4, 8: the taps unroll, every load of a thread is
+// issued before its FMA chains), 0 for the generic run-time radius.
+template <int RR>
+__global__ void k_conv_rows_base(const float *__restrict__ in, float *__restrict__ out, int n, int Rr, int W,
                                  RealConv c) {
+    const int R = RR ? RR : Rr;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int x0 = blockIdx.x * blockDim.x * W + threadIdx.x;
+    const float *row = in + (size_t)y * n;
     for (int q = 0; q < W; ++q) {
         const int x = x0 + q * blockDim.x;
         float acc = 0.0f;
+#pragma unroll
         for (int k = -R; k <= R; ++k) {
             const int xx = x + k;
-            const float v = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
+            const float v = (xx >= 0 && xx < n) ? __ldg(row + xx) : 0.0f;
             acc = __fmaf_rn(v, c.w[R - k], acc);
         }
         out[(size_t)y * n + x] = acc;
     }
 }
 
-__global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+template <int RR>
+__global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict__ out, int n, int Rr, int W,
                                  RealConv c) {
+    const int R = RR ? RR : Rr;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y0 = blockIdx.y * blockDim.y * W + threadIdx.y;
     for (int q = 0; q < W; ++q) {
         const int y = y0 + q * blockDim.y;
         float acc = 0.0f;
+#pragma unroll
         for (int k = -R; k <= R; ++k) {
             const int yy = y + k;
-            const float v = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
+            const float v = (yy >= 0 && yy < n) ? __ldg(in + (size_t)yy * n + x) : 0.0f;
             acc = __fmaf_rn(v, c.w[R - k], acc);
         }
         out[(size_t)y * n + x] = acc;
     }
 }
 
-// optimized: the CTA's rows (its W * wx columns plus the apron) staged once in shared memory
-__global__ void k_conv_rows_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+// optimized: the CTA's rows (its W * wx columns plus the apron) staged once in
+// shared memory; the interior is copied with 128-bit loads when aligned
+template <int RR>
+__global__ void k_conv_rows_opt(const float *__restrict__ in, float *__restrict__ out, int n, int Rr, int W,
                                 RealConv c) {
+    const int R = RR ? RR : Rr;
     extern __shared__ float s[];  // [wy][W * wx + 2R]
-    const int wx = blockDim.x, wy = blockDim.y, P = W * wx + 2 * R;
-    const int x0 = blockIdx.x * wx * W - R, y = blockIdx.y * wy + threadIdx.y;
-    for (int t = threadIdx.x; t < P; t += wx) {
-        const int xx = x0 + t;
-        s[threadIdx.y * P + t] = (xx >= 0 && xx < n) ? in[(size_t)y * n + xx] : 0.0f;
+    const int wx = blockDim.x, wy = blockDim.y, span = W * wx, P = span + 2 * R;
+    const int xb = blockIdx.x * span, y = blockIdx.y * wy + threadIdx.y;
+    const float *row = in + (size_t)y * n;
+    float *srow = s + threadIdx.y * P;
+    if ((span & 3) == 0 && (n & 3) == 0) {
+        for (int t = threadIdx.x; t < span / 4; t += wx) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(row + xb) + t);
+            srow[R + 4 * t + 0] = v.x;
+            srow[R + 4 * t + 1] = v.y;
+            srow[R + 4 * t + 2] = v.z;
+            srow[R + 4 * t + 3] = v.w;
+        }
+        for (int t = threadIdx.x; t < 2 * R; t += wx) {  // the two aprons
+            const int xx = t < R ? xb - R + t : xb + span + (t - R);
+            srow[t < R ? t : span + t] = (xx >= 0 && xx < n) ? row[xx] : 0.0f;
+        }
+    } else {
+        for (int t = threadIdx.x; t < P; t += wx) {
+            const int xx = xb - R + t;
+            srow[t] = (xx >= 0 && xx < n) ? row[xx] : 0.0f;
+        }
     }
     __syncthreads();
     for (int q = 0; q < W; ++q) {
         const int lx = threadIdx.x + q * wx;
         float acc = 0.0f;
-        for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[threadIdx.y * P + lx + R + k], c.w[R - k], acc);
-        out[(size_t)y * n + blockIdx.x * wx * W + lx] = acc;
+#pragma unroll
+        for (int k = -R; k <= R; ++k) acc = __fmaf_rn(srow[lx + R + k], c.w[R - k], acc);
+        out[(size_t)y * n + xb + lx] = acc;
     }
 }
 
-__global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict__ out, int n, int R, int W,
+template <int RR>
+__global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict__ out, int n, int Rr, int W,
                                 RealConv c) {
+    const int R = RR ? RR : Rr;
     extern __shared__ float s[];  // [W * wy + 2R][wx]
     const int wx = blockDim.x, wy = blockDim.y, H = W * wy + 2 * R;
     const int x = blockIdx.x * wx + threadIdx.x, y0 = blockIdx.y * wy * W - R;
     for (int t = threadIdx.y; t < H; t += wy) {
         const int yy = y0 + t;
-        s[t * wx + threadIdx.x] = (yy >= 0 && yy < n) ? in[(size_t)yy * n + x] : 0.0f;
+        s[t * wx + threadIdx.x] = (yy >= 0 && yy < n) ? __ldg(in + (size_t)yy * n + x) : 0.0f;
     }
     __syncthreads();
     for (int q = 0; q < W; ++q) {
         const int ly = threadIdx.y + q * wy;
         float acc = 0.0f;
+#pragma unroll
         for (int k = -R; k <= R; ++k) acc = __fmaf_rn(s[(ly + R + k) * wx + threadIdx.x], c.w[R - k], acc);
         out[(size_t)(blockIdx.y * wy * W + ly) * n + x] = acc;
     }
