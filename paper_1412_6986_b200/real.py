@@ -50,7 +50,7 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
     """The configs[1] instance set: 18 transpose (tile T in {8,16,32} x rows
     per CTA step, and 64 x 64 tiles with two columns per thread), 14 matrixMul (T in {4..32} x outputs per thread), 24
     convolution (radius in {1,2,4,8} x 6 workgroups), 10 MVT (workgroup x
-    j-tile), plus 7 transpose and 8 convolution instances at 8192 x 8192
+    j-tile), plus 9 transpose and 8 convolution instances at 8192 x 8192
     (arrays well beyond L2) for the HBM roof."""
     out = []
     for T in (8, 16, 32):
@@ -75,6 +75,8 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
     out.append(RealInstance(0, 8192, 16, 16, tile=16))
     for wy in (4, 8):
         out.append(RealInstance(0, 8192, 32, wy, tile=64))
+    for wy in (8, 16):  # four columns per thread (128-bit loads and stores)
+        out.append(RealInstance(0, 8192, 16, wy, tile=64))
     for R in (1, 2, 4, 8):
         for W in (1, 4):  # outputs per thread
             out.append(RealInstance(2, 8192, 32, 8, tile=W, radius=R))
