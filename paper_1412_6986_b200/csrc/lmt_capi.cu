@@ -1779,7 +1779,8 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
             } else {
                 // A streamed through a ring of S stages of [wg][T] (kernel 1, swizzled
                 // 64/128-byte rows) and [T][wg] (kernel 2) tiles by TMA
-                const int64_t stage = (int64_t)wx * T * 4, cap = smem_optin - 2048;
+                // y is staged whole in shared memory after each kernel's ring
+                const int64_t stage = (int64_t)wx * T * 4, cap = smem_optin - 2048 - (int64_t)n * 4;
                 const int S = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage, (int64_t)n / T});
                 // kernel 1: stages of up to 256 columns (KB boxes of T), two of them at least when they fit
                 int KB = kMvtStageCols / T;
@@ -1805,11 +1806,12 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                     return fail(LMT_ERR_CUDA, "MVT tensor maps: %d %d", (int)e1, (int)e2);
                 const RealTmap t1 = *reinterpret_cast<const RealTmap *>(&m1);
                 const RealTmap t2 = *reinterpret_cast<const RealTmap *>(&m2);
-                if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 1024, s>>>(t1, in[1], in[3], out, n, S1, KB);
-                else k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 1024, s>>>(t1, in[1], in[3], out, n, S1, KB);
+                const size_t ybytes = (size_t)n * 4;
+                if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 1024 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, KB);
+                else k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 1024 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, KB);
                 CUDA_TRY(cudaGetLastError());
-                if (T == 32) k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, S);
-                else k_mvt2_tma<16><<<grd, wx, (size_t)S * stage + 128, s>>>(t2, in[2], in[4], out + n, n, S);
+                if (T == 32) k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
+                else k_mvt2_tma<16><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
             }
             break;
         }

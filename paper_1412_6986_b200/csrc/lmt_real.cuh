@@ -414,61 +414,83 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
     const int swz = T == 32 ? (tid & 7) : ((tid >> 1) & 3);
     float acc = x1_0[i0 + tid];
     const unsigned base = rk_smem(st) + (unsigned)(tid * T * 4);
-    const float4 *y4 = reinterpret_cast<const float4 *>(y1);
-    float4 ca[T / 4], cy[T / 4], na[T / 4], ny[T / 4];
-    // sub-step k = (stage k / KB, box kb = k % KB): its T columns are j = k * T ..
-    auto load = [&](float4 (&a)[T / 4], float4 (&y)[T / 4], int slot, int kb, int k) {
-        const unsigned bx = base + (unsigned)((slot * sf + kb * wg * T) * 4);
-#pragma unroll
-        for (int c = 0; c < T / 4; ++c) {
-            a[c] = rk_lds4(bx + (unsigned)((c ^ swz) << 4));
-            y[c] = __ldg(y4 + k * (T / 4) + c);
-        }
-    };
+    // y (the same for every lane) is staged whole in shared memory after the
+    // ring and read at use: an LDS broadcast the compiler hoists ahead of the chain
+    float *ys = st + (size_t)S * sf;
+    for (int j = tid; j < n; j += wg) ys[j] = __ldg(y1 + j);
+    __syncthreads();
+    const unsigned ybase = rk_smem(ys);
+    // two register buffers, ping-pong: sub-step k = (stage k / KB, box k % KB)
+    // computes from one while the other receives sub-step k + 1
+    float4 a0[T / 4], a1[T / 4];
     const int total = steps * KB;
-    rk_wait(&full[0], 0);
-    load(ca, cy, 0, 0, 0);
     int slot = 0, kb = 0, step = 0;
     unsigned phase = 0;
-    for (int k = 0; k < total; ++k) {
-        const bool last = kb == KB - 1;  // the stage's last box
-        int ns = slot;
-        unsigned nph = phase;
-        if (last && ++ns == S) {
-            ns = 0;
-            nph ^= 1;
-        }
-        if (k + 1 < total) {
-            if (last) rk_wait(&full[ns], nph);
-            load(na, ny, ns, last ? 0 : kb + 1, k + 1);
-        }
-#pragma unroll
-        for (int c = 0; c < T / 4; ++c) {
-            acc = __fmaf_rn(ca[c].x, cy[c].x, acc);
-            acc = __fmaf_rn(ca[c].y, cy[c].y, acc);
-            acc = __fmaf_rn(ca[c].z, cy[c].z, acc);
-            acc = __fmaf_rn(ca[c].w, cy[c].w, acc);
-        }
-        if (last) {
-            __syncwarp();
-            if (lane == 0) rk_arrive(&empty[slot]);
-            if (tid == 0 && step + S < steps) {
-                rk_wait(&empty[slot], phase);
-                issue(slot, step + S);
-            }
-            ++step;
-            kb = 0;
-        } else {
-            ++kb;
-        }
-#pragma unroll
-        for (int c = 0; c < T / 4; ++c) {
-            ca[c] = na[c];
-            cy[c] = ny[c];
-        }
-        slot = ns;
-        phase = nph;
+    // where sub-step k + 1 lives, advancing the ring when k closes a stage
+#define MVT1_NEXT(ns, nph, nkb, last) \
+    const bool last = kb == KB - 1;   \
+    int ns = slot;                    \
+    unsigned nph = phase;             \
+    if (last && ++ns == S) {          \
+        ns = 0;                       \
+        nph ^= 1;                     \
+    }                                 \
+    const int nkb = last ? 0 : kb + 1;
+#define MVT1_LOAD(A, sl, bk)                                                    \
+    {                                                                           \
+        const unsigned bx = base + (unsigned)(((sl) * sf + (bk) * wg * T) * 4); \
+        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) A[c] = rk_lds4(bx + (unsigned)((c ^ swz) << 4)); \
     }
+#define MVT1_FMA(A, kk)                                 \
+    _Pragma("unroll") for (int c = 0; c < T / 4; ++c) { \
+        const float4 yv = rk_lds4(ybase + (unsigned)(((kk) * T + 4 * c) * 4)); \
+        acc = __fmaf_rn(A[c].x, yv.x, acc);             \
+        acc = __fmaf_rn(A[c].y, yv.y, acc);             \
+        acc = __fmaf_rn(A[c].z, yv.z, acc);             \
+        acc = __fmaf_rn(A[c].w, yv.w, acc);             \
+    }
+#define MVT1_RELEASE(last)                      \
+    if (last) {                                 \
+        __syncwarp();                           \
+        if (lane == 0) rk_arrive(&empty[slot]); \
+        if (tid == 0 && step + S < steps) {     \
+            rk_wait(&empty[slot], phase);       \
+            issue(slot, step + S);              \
+        }                                       \
+        ++step;                                 \
+    }
+    rk_wait(&full[0], 0);
+    MVT1_LOAD(a0, 0, 0)
+    for (int k = 0; k < total; k += 2) {
+        {  // sub-step k from buffer 0, k + 1 into buffer 1
+            MVT1_NEXT(ns, nph, nkb, last)
+            if (k + 1 < total) {
+                if (last) rk_wait(&full[ns], nph);
+                MVT1_LOAD(a1, ns, nkb)
+            }
+            MVT1_FMA(a0, k)
+            MVT1_RELEASE(last)
+            slot = ns;
+            phase = nph;
+            kb = nkb;
+        }
+        if (k + 1 < total) {  // sub-step k + 1 from buffer 1, k + 2 into buffer 0
+            MVT1_NEXT(ns, nph, nkb, last)
+            if (k + 2 < total) {
+                if (last) rk_wait(&full[ns], nph);
+                MVT1_LOAD(a0, ns, nkb)
+            }
+            MVT1_FMA(a1, k + 1)
+            MVT1_RELEASE(last)
+            slot = ns;
+            phase = nph;
+            kb = nkb;
+        }
+    }
+#undef MVT1_NEXT
+#undef MVT1_LOAD
+#undef MVT1_FMA
+#undef MVT1_RELEASE
     x1[i0 + tid] = acc;
 }
 
@@ -500,14 +522,17 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
     const int b = tid / bcols, c = tid - b * bcols;
     float acc = x2_0[i0 + tid];
     const unsigned base = rk_smem(st) + (unsigned)((b * T * bcols + c) * 4);
-    const float4 *y4 = reinterpret_cast<const float4 *>(y2);
+    float *ysm = st + (size_t)S * sf;  // y, whole, after the ring (LDS broadcasts)
+    for (int j = tid; j < n; j += wg) ysm[j] = __ldg(y2 + j);
+    __syncthreads();
+    const unsigned ybase = rk_smem(ysm);
     float ca[T], na[T];
     float4 cy[T / 4], ny[T / 4];
     auto load = [&](float (&a)[T], float4 (&y)[T / 4], int slot, int step) {
 #pragma unroll
         for (int jj = 0; jj < T; ++jj) a[jj] = rk_lds(base + (unsigned)((slot * sf + jj * bcols) * 4));
 #pragma unroll
-        for (int q = 0; q < T / 4; ++q) y[q] = __ldg(y4 + step * (T / 4) + q);
+        for (int q = 0; q < T / 4; ++q) y[q] = rk_lds4(ybase + (unsigned)((step * T + 4 * q) * 4));
     };
     rk_wait(&full[0], 0);
     load(ca, cy, 0, 0);
