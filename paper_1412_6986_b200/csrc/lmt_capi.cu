@@ -252,6 +252,8 @@ struct Lane {
     // sets, so the copies of instances i +- 1 overlap the kernels of i
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t copied[2] = {}, consumed[2] = {}, drained[2] = {};
+    CUgreenCtx gctx = nullptr;  // the partition's green context (copy streams are created in it)
+    unsigned seq = 0;           // instances enqueued on this lane (buffer set = seq & 1)
     std::vector<int64_t> inflight;  // instances enqueued, in order
 };
 
@@ -307,8 +309,17 @@ int ensure(T **p, size_t *cap, size_t need) {
 
 int lane_streams(Lane &L) {
     if (L.h2d) return LMT_OK;
-    CUDA_TRY(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
-    CUDA_TRY(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
+    if (L.gctx) {  // a partition: its copy streams live in its green context too
+        CUstream a, b;
+        if (g_green.stream_create(&a, L.gctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+            g_green.stream_create(&b, L.gctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+            return fail(LMT_ERR_CUDA, "green-context copy streams");
+        L.h2d = (cudaStream_t)a;
+        L.d2h = (cudaStream_t)b;
+    } else {
+        CUDA_TRY(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
+    }
     for (int b = 0; b < 2; b++) {
         CUDA_TRY(cudaEventCreateWithFlags(&L.copied[b], cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&L.consumed[b], cudaEventDisableTiming));
@@ -426,6 +437,7 @@ int ensure_parts(DevCtx *c) {
         Lane L;
         L.sms = (int)(k * per);
         L.s = (cudaStream_t)st;
+        L.gctx = gc;
         if (g_green.to_ctx(&L.ctx, gc) != CUDA_SUCCESS) break;
         int rc = warm_lane(L);
         if (rc) return rc;
@@ -975,8 +987,10 @@ int enqueue(DevCtx *c, Batch &B, Lane &L, int64_t i) {
     const int64_t pitch = round_up(cols, 4);
     const size_t need_in = need_in_elems(B, i, pl), need_out = (size_t)p.out_h * p.out_w;
     const bool ropt = run_opt_of(B, pl, c);
-    const bool pipelined = whole && B.host();  // copies on their own streams, two buffer sets
-    const int b = pipelined ? (int)(i & 1) : 0;
+    // host buffers: copies on the lane's own copy streams, two buffer sets, so
+    // the copies of the lane's neighbouring instances overlap its kernels
+    const bool pipelined = B.host();
+    const int b = pipelined ? (int)(L.seq++ & 1) : 0;
     int rc;
     if (pipelined && (rc = lane_streams(L))) return rc;
     // ---- buffers (growing one waits for everything in flight on the lane)
@@ -1323,8 +1337,10 @@ int measure_run(Batch &B) {
         }
         if (!progressed) std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
-    for (Lane &L : c->parts)
+    for (Lane &L : c->parts) {
         if ((rc = retire(c, L, true))) return rc;
+        if (L.d2h) CUDA_TRY(cudaStreamSynchronize(L.d2h));
+    }
     if ((rc = retire(c, c->full, true))) return rc;
     if (c->full.d2h) CUDA_TRY(cudaStreamSynchronize(c->full.d2h));
     // ---- results
