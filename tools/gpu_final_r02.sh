@@ -31,3 +31,12 @@ timeout 900 python tools/real_summary.py $OUT/real_summary.json > $OUT/real_summ
 bash tools/sanitize.sh ${TAG}_san > /dev/null 2>&1
 for f in $OUT/pytest_gpu.log $OUT/smoke.log $OUT/bench.err; do tail -n 2 $f; done
 cat $OUT/real_summary.txt; head -c 1500 $OUT/bench.json; echo; head -c 600 $OUT/bench_reference.json
+# K3 / K4 / GPU RF training and K5 under ncu
+timeout 900 ncu --set full --clock-control none -k regex:"k_rf_mean|k_features|k_rf_build|k_rf_presort" -c 6 \
+    -o $OUT/prof_rf python tools/ncu_rf.py > $OUT/ncu_rf.log 2>&1
+ncu -i $OUT/prof_rf.ncu-rep --page details --csv > $OUT/details_rf.csv 2>&1
+mv $OUT/prof_rf.ncu-rep /tmp/ 2>/dev/null
+timeout 900 ncu --set full --clock-control none -k regex:"k_mvt|k_transpose|k_conv|k_matmul" \
+    -o $OUT/prof_real python tools/ncu_real.py 0,8192,16,16,64,0 1,1024,32,4,32,0 2,8192,32,8,4,1 3,4096,32,1,32,0 > $OUT/ncu_real.log 2>&1
+ncu -i $OUT/prof_real.ncu-rep --page details --csv > $OUT/details_real.csv 2>&1
+mv $OUT/prof_real.ncu-rep /tmp/ 2>/dev/null
