@@ -373,6 +373,27 @@ __device__ __forceinline__ float rk_lds(unsigned a) {
 }
 constexpr int kMvtMaxStages = 16;
 
+// Copy a vector of n floats (n % 4 == 0, both 16-byte aligned) to shared
+// memory: 128-bit loads, eight in flight per thread (a serial load -> store
+// loop would pay one global latency per element of the thread).
+__device__ __forceinline__ void rk_stage_vec(float *dst, const float *src, int n, int tid, int nthreads) {
+    const float4 *s4 = reinterpret_cast<const float4 *>(src);
+    const unsigned d = rk_smem(dst);
+    const int n4 = n >> 2;
+    for (int q0 = tid; q0 < n4; q0 += 8 * nthreads) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (q0 + u * nthreads < n4) v[u] = __ldg(s4 + q0 + u * nthreads);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (q0 + u * nthreads < n4)
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d + (unsigned)((q0 + u * nthreads) * 16)),
+                             "f"(v[u].x), "f"(v[u].y), "f"(v[u].z), "f"(v[u].w)
+                             : "memory");
+    }
+}
+
 // Kernel 1: a ring of S stages, each 256 columns of the CTA's wg rows as
 // 256 / T boxes of T columns (1 KB of every row per stage, so DRAM sees
 // row segments of 1 KB rather than 128 B); the boxes' 64/128-byte rows are
@@ -417,7 +438,7 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
     // y (the same for every lane) is staged whole in shared memory after the
     // ring and read at use: an LDS broadcast the compiler hoists ahead of the chain
     float *ys = st + (size_t)S * sf;
-    for (int j = tid; j < n; j += wg) ys[j] = __ldg(y1 + j);
+    rk_stage_vec(ys, y1, n, tid, wg);
     __syncthreads();
     const unsigned ybase = rk_smem(ys);
     // two register buffers, ping-pong: sub-step k = (stage k / KB, box k % KB)
@@ -523,7 +544,7 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
     float acc = x2_0[i0 + tid];
     const unsigned base = rk_smem(st) + (unsigned)((b * T * bcols + c) * 4);
     float *ysm = st + (size_t)S * sf;  // y, whole, after the ring (LDS broadcasts)
-    for (int j = tid; j < n; j += wg) ysm[j] = __ldg(y2 + j);
+    rk_stage_vec(ysm, y2, n, tid, wg);
     __syncthreads();
     const unsigned ybase = rk_smem(ysm);
     float ca[T], na[T];
