@@ -394,27 +394,36 @@ __device__ __forceinline__ void rk_stage_vec(float *dst, const float *src, int n
     }
 }
 
-// Kernel 1: a ring of S stages, each 256 columns of the CTA's wg rows as
-// 256 / T boxes of T columns (1 KB of every row per stage, so DRAM sees
-// row segments of 1 KB rather than 128 B); the boxes' 64/128-byte rows are
-// TMA-swizzled (64B/128B modes) so that a quarter-warp's 128-bit reads of 8
-// rows hit 8 distinct bank groups. Kernel 2: stages of T rows x wg columns,
-// read one float per lane (consecutive). Thread 0 issues the TMA loads and
-// refills a stage once every warp released it; each thread's registers hold
-// the next box (kernel 1) / stage (kernel 2) while the current one's FMAs
-// run -- one warp per SM carries the serial chains, so latency is the limit.
+__device__ __forceinline__ void rk_bulk(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     rk_smem(dst)),
+                 "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(rk_smem(bar))
+                 : "memory");
+}
+
+// Kernel 1 (row dots): a ring of S stages, each SC columns (256, fewer for
+// wide workgroups) of the CTA's wg rows, one 1D bulk copy (cp.async.bulk,
+// the TMA engine) per row segment -- 1 KB requests instead of the 128-byte
+// rows of a 2D box -- into rows padded by 16 bytes, so a quarter-warp's
+// 128-bit reads of 8 rows hit 8 distinct bank groups. Warp 0 issues the
+// copies (expect_tx first, then one row per lane) and refills a stage once
+// every warp released it. Kernel 2 (column dots): stages of T rows x wg
+// columns by 2D TMA boxes, read one float per lane (consecutive). Each
+// thread's registers hold the next sub-step (kernel 1) / stage (kernel 2)
+// while the current FMAs run: one warp per SM carries the serial chains, so
+// latency is the limit.
 constexpr int kMvtStageCols = 256;
 template <int T>
-__global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y1,
-                                                  const float *__restrict__ x1_0, float *__restrict__ x1, int n,
-                                                  int S, int KB) {
-    // KB boxes of T columns per stage (kMvtStageCols columns, fewer for wide workgroups)
+__global__ void __launch_bounds__(512) k_mvt1_bulk(const float *__restrict__ A, const float *__restrict__ y1,
+                                                   const float *__restrict__ x1_0, float *__restrict__ x1, int n,
+                                                   int S, int SC) {
     extern __shared__ unsigned char rk_raw[];
     __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
-    float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 1023) & ~uintptr_t(1023));
-    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
-    const int i0 = blockIdx.x * wg, steps = n / (KB * T), sf = wg * KB * T;
-    const int boxes = (wg + 255) / 256, brows = wg < 256 ? wg : 256;
+    float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
+    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int i0 = blockIdx.x * wg, steps = n / SC, KB = SC / T;
+    const int pitch = SC + 4;        // floats per staged row (+16 bytes: rows rotate through the bank groups)
+    const int sf = wg * pitch;       // floats per stage
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             rk_bar_init(&full[s], 1);
@@ -423,31 +432,29 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // warp 0 only: lane 0 arms the barrier for the stage's bytes, then every
+    // lane copies its rows
     auto issue = [&](int slot, int step) {
-        rk_expect(&full[slot], (unsigned)(sf * 4));
-        for (int kb = 0; kb < KB; ++kb)
-            for (int b = 0; b < boxes; ++b)
-                rk_tma2d(st + slot * sf + kb * wg * T + b * 256 * T, &tm, &full[slot], (step * KB + kb) * T,
-                         i0 + b * brows);
+        if (lane == 0) rk_expect(&full[slot], (unsigned)(wg * SC * 4));
+        __syncwarp();
+        for (int r = lane; r < wg; r += 32)
+            rk_bulk(st + slot * sf + r * pitch, A + (size_t)(i0 + r) * n + (size_t)step * SC, (unsigned)(SC * 4),
+                    &full[slot]);
     };
-    if (tid == 0)
+    if (warp == 0)
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
-    const int swz = T == 32 ? (tid & 7) : ((tid >> 1) & 3);
-    float acc = x1_0[i0 + tid];
-    const unsigned base = rk_smem(st) + (unsigned)(tid * T * 4);
-    // y (the same for every lane) is staged whole in shared memory after the
-    // ring and read at use: an LDS broadcast the compiler hoists ahead of the chain
-    float *ys = st + (size_t)S * sf;
+    float *ys = st + (size_t)S * sf;  // y, whole, after the ring: LDS broadcasts
     rk_stage_vec(ys, y1, n, tid, wg);
     __syncthreads();
     const unsigned ybase = rk_smem(ys);
-    // two register buffers, ping-pong: sub-step k = (stage k / KB, box k % KB)
-    // computes from one while the other receives sub-step k + 1
+    float acc = x1_0[i0 + tid];
+    const unsigned base = rk_smem(st) + (unsigned)(tid * pitch * 4);
+    // two register buffers, ping-pong: sub-step k = (stage k / KB, T-column
+    // slice k % KB) computes from one while the other receives k + 1
     float4 a0[T / 4], a1[T / 4];
     const int total = steps * KB;
     int slot = 0, kb = 0, step = 0;
     unsigned phase = 0;
-    // where sub-step k + 1 lives, advancing the ring when k closes a stage
 #define MVT1_NEXT(ns, nph, nkb, last) \
     const bool last = kb == KB - 1;   \
     int ns = slot;                    \
@@ -457,28 +464,29 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
         nph ^= 1;                     \
     }                                 \
     const int nkb = last ? 0 : kb + 1;
-#define MVT1_LOAD(A, sl, bk)                                                    \
-    {                                                                           \
-        const unsigned bx = base + (unsigned)(((sl) * sf + (bk) * wg * T) * 4); \
-        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) A[c] = rk_lds4(bx + (unsigned)((c ^ swz) << 4)); \
+#define MVT1_LOAD(A_, sl, bk)                                                          \
+    {                                                                                  \
+        const unsigned bx = base + (unsigned)(((sl) * sf + (bk) * T) * 4);             \
+        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) A_[c] = rk_lds4(bx + (unsigned)(c << 4)); \
     }
-#define MVT1_FMA(A, kk)                                 \
-    _Pragma("unroll") for (int c = 0; c < T / 4; ++c) { \
+#define MVT1_FMA(A_, kk)                                                       \
+    _Pragma("unroll") for (int c = 0; c < T / 4; ++c) {                        \
         const float4 yv = rk_lds4(ybase + (unsigned)(((kk) * T + 4 * c) * 4)); \
-        acc = __fmaf_rn(A[c].x, yv.x, acc);             \
-        acc = __fmaf_rn(A[c].y, yv.y, acc);             \
-        acc = __fmaf_rn(A[c].z, yv.z, acc);             \
-        acc = __fmaf_rn(A[c].w, yv.w, acc);             \
+        acc = __fmaf_rn(A_[c].x, yv.x, acc);                                   \
+        acc = __fmaf_rn(A_[c].y, yv.y, acc);                                   \
+        acc = __fmaf_rn(A_[c].z, yv.z, acc);                                   \
+        acc = __fmaf_rn(A_[c].w, yv.w, acc);                                   \
     }
-#define MVT1_RELEASE(last)                      \
-    if (last) {                                 \
-        __syncwarp();                           \
-        if (lane == 0) rk_arrive(&empty[slot]); \
-        if (tid == 0 && step + S < steps) {     \
-            rk_wait(&empty[slot], phase);       \
-            issue(slot, step + S);              \
-        }                                       \
-        ++step;                                 \
+#define MVT1_RELEASE(last)                                \
+    if (last) {                                           \
+        __syncwarp();                                     \
+        if (lane == 0) rk_arrive(&empty[slot]);           \
+        if (warp == 0 && step + S < steps) {              \
+            if (lane == 0) rk_wait(&empty[slot], phase);  \
+            __syncwarp();                                 \
+            issue(slot, step + S);                        \
+        }                                                 \
+        ++step;                                           \
     }
     rk_wait(&full[0], 0);
     MVT1_LOAD(a0, 0, 0)
