@@ -23,13 +23,13 @@ for k, r in enumerate(recs):
                                                   "opt_ms": float(np.median(m["t_opt_ms"])),
                                                   "kid": int(m["kernel_id"][0]), "G": int(m["nstages"][0])},
                    "base": [], "opt": []}
-for U, D, mb in itertools.product((1, 2, 4, 8, 16), (1, 2, 3), (0, 2, 4, 8)):
+for U, D, mb in itertools.product((2, 4, 8, 16), (1, 3), (0, 4, 8)):
     res = L.measure_records(np.repeat(recs, reps, axis=0), tune=(U, D, mb, 0, 0, 0), skip_opt=True)
     for k in range(len(recs)):
         m = res[k * reps:(k + 1) * reps]
         ok = bool((m["digest_base"] == auto["digest_base"][k * reps]).all()) and bool((m["status"] == 0).all())
         out[str(k)]["base"].append({"U": U, "D": D, "minb": mb, "ms": float(np.median(m["t_base_ms"])), "ok": ok})
-for U, G, mb in itertools.product((1, 2, 4, 8), (1, 2, 3), (0, 2, 4)):
+for U, G, mb in itertools.product((1, 2, 4, 8), (1, 2), (0, 4)):
     res = L.measure_records(np.repeat(recs, reps, axis=0), tune=(0, 0, 0, U, G, mb))
     for k in range(len(recs)):
         m = res[k * reps:(k + 1) * reps]
