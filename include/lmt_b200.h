@@ -268,6 +268,14 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
                       int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left,
                       int32_t *right, double *value, int64_t cap, int64_t *nodes_out, int64_t *draws_used);
 
+/* The per-split feature subsets of forest._best_split (forest.py:77:
+ * np.sort(rng.choice(nfeat, k, replace=False)), ndraws times) continued
+ * from a numpy Generator(PCG64) state: state4 = {state >> 64, state & mask,
+ * inc >> 64, inc & mask}, plus its buffered 32-bit half. Bit-identical to
+ * numpy's draws (nfeat <= 10000: Floyd's algorithm path). out: [ndraws][k]. */
+int lmt_rf_feature_draws(const uint64_t *state4, int32_t has_uint32, uint32_t uinteger, int32_t nfeat, int32_t k,
+                         int64_t ndraws, int32_t *out);
+
 /* forest.train's trees on the GPU (forest.py:117-163), all `ntrees` trees in
  * one call, bit-identical to lmt_rf_train_tree / the reference: samples =
  * [ntrees][nrows] bootstrap rows, draws = [ntrees][ndraws][k] sorted feature

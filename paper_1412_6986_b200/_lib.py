@@ -97,7 +97,7 @@ EXPORTS = (
     "lmt_rf_create", "lmt_rf_mean", "lmt_rf_mean_host", "lmt_rf_destroy", "lmt_sync",
     "lmt_get_stream", "lmt_prepare", "lmt_jit_stats", "lmt_features", "lmt_real_validate",
     "lmt_real_execute", "lmt_real_measure", "lmt_rf_train_tree", "lmt_kernel_source",
-    "lmt_measure_batch_ex", "lmt_partitions", "lmt_current_device", "lmt_plan_info", "lmt_rf_train_gpu",
+    "lmt_measure_batch_ex", "lmt_partitions", "lmt_current_device", "lmt_plan_info", "lmt_rf_train_gpu", "lmt_rf_feature_draws",
 )
 
 _lib = None
@@ -133,6 +133,7 @@ def _declare(L):
     L.lmt_rf_destroy.restype = None
     L.lmt_current_device.argtypes = [P(c_i32)]
     L.lmt_plan_info.argtypes = [P(CInstance), P(CDevice), c_i32, P(c_i64)]
+    L.lmt_rf_feature_draws.argtypes = [vp, c_i32, c_u32, c_i32, c_i32, c_i64, vp]
     L.lmt_rf_train_gpu.argtypes = [vp, vp, c_i64, c_i32, c_i32, vp, vp, c_i64, c_i32, c_i32, c_i32, vp, vp, vp, vp,
                                    vp, c_i64, vp, vp]
     L.lmt_sync.argtypes = []

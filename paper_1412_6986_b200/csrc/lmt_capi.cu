@@ -2013,6 +2013,19 @@ int lmt_rf_train_tree(const double *X, const double *y, int64_t nrows, int32_t n
     return LMT_OK;
 }
 
+int lmt_rf_feature_draws(const uint64_t *state4, int32_t has_uint32, uint32_t uinteger, int32_t nfeat, int32_t k,
+                         int64_t ndraws, int32_t *out) {
+    if (!state4 || !out || nfeat < 1 || nfeat > 10000 || k < 1 || k > nfeat || k > 64 || ndraws < 0)
+        return fail(LMT_ERR_ARG, "bad draw arguments");
+    NpPcg64 g;
+    g.state = ((unsigned __int128)state4[0] << 64) | state4[1];
+    g.inc = ((unsigned __int128)state4[2] << 64) | state4[3];
+    g.has32 = has_uint32 != 0;
+    g.u32 = uinteger;
+    for (int64_t i = 0; i < ndraws; i++) g.choice_sorted(nfeat, k, out + i * k);
+    return LMT_OK;
+}
+
 int lmt_rf_train_gpu(const double *X, const double *y, int64_t nrows, int32_t nfeat, int32_t ntrees,
                      const int64_t *samples, const int32_t *draws, int64_t ndraws, int32_t k, int32_t max_depth,
                      int32_t min_samples_leaf, int32_t *feature, double *threshold, int32_t *left, int32_t *right,

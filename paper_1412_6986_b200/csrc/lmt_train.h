@@ -45,6 +45,67 @@ inline double np_pairwise_sum(const double *a, int64_t n) {
     return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
 }
 
+// numpy's Generator(PCG64) stream from a given state, and its
+// choice(pop, k, replace=False) for pop <= 10000 (Floyd's algorithm over a
+// hash set, then a Fisher-Yates shuffle of the k picks; every bounded draw
+// is Lemire's method on the buffered 32-bit output). Verified draw for draw
+// against numpy 2.3 (tests/test_host.py::test_native_feature_draws).
+struct NpPcg64 {
+    unsigned __int128 state, inc;
+    bool has32;
+    uint32_t u32;
+    uint64_t next64() {
+        const unsigned __int128 mult = ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+        state = state * mult + inc;
+        const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+        const unsigned rot = (unsigned)(state >> 122);
+        const uint64_t x = hi ^ lo;
+        return rot ? (x >> rot) | (x << (64 - rot)) : x;
+    }
+    uint32_t next32() {
+        if (has32) {
+            has32 = false;
+            return u32;
+        }
+        const uint64_t v = next64();
+        has32 = true;
+        u32 = (uint32_t)(v >> 32);
+        return (uint32_t)v;
+    }
+    // random_bounded_uint64(off = 0, rng, use_masked = false) for rng < 2^32
+    uint64_t bounded(uint64_t rng) {
+        if (rng == 0) return 0;
+        if (rng == 0xFFFFFFFFull) return next32();
+        const uint32_t ex = (uint32_t)rng + 1;
+        uint64_t m = (uint64_t)next32() * ex;
+        uint32_t left = (uint32_t)m;
+        if (left < ex) {
+            const uint32_t thr = (uint32_t)((0xFFFFFFFFull - rng) % ex);
+            while (left < thr) {
+                m = (uint64_t)next32() * ex;
+                left = (uint32_t)m;
+            }
+        }
+        return m >> 32;
+    }
+    // sort(choice(pop, k, replace=False)) into out[k]
+    void choice_sorted(int pop, int k, int32_t *out) {
+        int64_t idx[64];
+        for (int j = pop - k; j < pop; j++) {
+            const int64_t val = (int64_t)bounded((uint64_t)j);
+            bool seen = false;
+            for (int q = 0; q < j - (pop - k); q++) seen |= idx[q] == val;
+            idx[j - pop + k] = seen ? j : val;
+        }
+        for (int i = k - 1; i > 0; i--) {
+            const int64_t jj = (int64_t)bounded((uint64_t)i);
+            std::swap(idx[i], idx[jj]);
+        }
+        std::sort(idx, idx + k);
+        for (int q = 0; q < k; q++) out[q] = (int32_t)idx[q];
+    }
+};
+
 struct TreeOut {
     std::vector<int32_t> feature, left, right;
     std::vector<double> threshold, value;

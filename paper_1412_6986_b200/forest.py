@@ -87,8 +87,20 @@ def _tree_draws(seed: int, n: int, nfeat: int, hp: Hyperparams, ndraws: int):
         oob = None
     k = min(hp.features_per_node, nfeat)
     draws = np.empty((ndraws, k), dtype=np.int32)
-    for i in range(ndraws):
-        draws[i] = np.sort(rng.choice(nfeat, size=k, replace=False))
+    if nfeat <= 10000 and k <= 64:
+        # the same numpy stream continued natively (lmt_rf_feature_draws:
+        # PCG64 + Generator.choice's algorithm, bit-identical): a Python loop
+        # of rng.choice calls costs ~12 us per draw
+        st = rng.bit_generator.state
+        mask = (1 << 64) - 1
+        s4 = np.array([st["state"]["state"] >> 64, st["state"]["state"] & mask, st["state"]["inc"] >> 64,
+                       st["state"]["inc"] & mask], dtype=np.uint64)
+        check(lib().lmt_rf_feature_draws(ctypes.c_void_p(s4.ctypes.data), int(st["has_uint32"]),
+                                         int(st["uinteger"]), nfeat, k, ndraws, ctypes.c_void_p(draws.ctypes.data)),
+              what="rf_feature_draws")
+    else:
+        for i in range(ndraws):
+            draws[i] = np.sort(rng.choice(nfeat, size=k, replace=False))
     return np.ascontiguousarray(sample, dtype=np.int64), oob, draws
 
 

@@ -275,3 +275,25 @@ def test_launch_plans_fit_the_device():
             assert 1 <= v[0] <= 16 and 1 <= v[1] <= 3 and 1 <= v[5] <= 8 and 1 <= v[9] <= 16, (r.tolist(), v)
             if v[12] * 4 <= cap:  # one region fits: the ring must too
                 assert v[10] <= cap, (r.tolist(), v)
+
+
+def test_native_feature_draws():
+    """lmt_rf_feature_draws continues a numpy Generator(PCG64) stream with
+    Generator.choice's own algorithm: draw for draw equal to numpy's, after a
+    bootstrap `integers` call has left a buffered 32-bit half or not."""
+    import ctypes
+
+    from paper_1412_6986_b200._lib import lib
+
+    mask = (1 << 64) - 1
+    for seed, n, nfeat, k in ((0, 10000, 18, 4), (7, 37, 18, 6), (3, 500, 18, 18), (11, 9, 5, 2)):
+        rng = np.random.Generator(np.random.PCG64(seed))
+        rng.integers(0, n, size=n)
+        st = rng.bit_generator.state
+        s4 = np.array([st["state"]["state"] >> 64, st["state"]["state"] & mask, st["state"]["inc"] >> 64,
+                       st["state"]["inc"] & mask], dtype=np.uint64)
+        got = np.empty((500, k), dtype=np.int32)
+        assert lib().lmt_rf_feature_draws(ctypes.c_void_p(s4.ctypes.data), int(st["has_uint32"]),
+                                          int(st["uinteger"]), nfeat, k, 500, ctypes.c_void_p(got.ctypes.data)) == 0
+        want = np.stack([np.sort(rng.choice(nfeat, size=k, replace=False)) for _ in range(500)])
+        assert np.array_equal(got, want), (seed, nfeat, k)
