@@ -624,6 +624,19 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
             if (bd > 1) bd--;
             else { bu >>= 1; bd = 3; }
         }
+        // Launches of many 1-2-warp CTAs: resident warps hide latency better
+        // than a deep prefetch ring once fewer than 16 warps per SM would fit
+        // (measured on B200, tools/tune_records.py, profiles/r02_tune_top.json:
+        // a 131,072-CTA launch of 2-thread workgroups, D = 3 -> 1: 143 -> 119 ms).
+        auto resident = [&](int U, int D) {
+            // ptxas allocates ~1.45x the live-value estimate (address registers, temporaries)
+            const int64_t regs = std::min<int64_t>(255, ((int64_t)(1.45 * est(U, D)) + 7) / 8 * 8);
+            const int64_t ctas_sm = std::min<int64_t>({32, 64 / std::max<int64_t>(1, warps),
+                                                       65536 / std::max<int64_t>(1, regs * 32 * warps)});
+            return ctas_sm * warps;
+        };
+        if (warps <= 2 && ctas >= 2 * sms * (16 / warps))
+            while (bd > 1 && resident(bu, bd) < 16) bd--;
     } else {
         bd = std::min(2, dmax);  // shared-memory loads: one step of lookahead covers them
         bu = 1;  // when no shape fits (the region alone exceeds shared memory) the variant is infeasible
@@ -646,7 +659,11 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
                 const double chains = std::min(64.0, (double)act * (double)warps * U / 4.0);
                 // two stages: the next group's regions land while this one computes
                 const bool overlap = G >= 2 || ngroups(U) == 1;
-                const double score = chains * 64.0 + (overlap ? 16.0 : 0.0) + U * 2.0;
+                // stagings in flight per SM (resident CTAs x stages): with one CTA and one
+                // stage every group waits out its own TMA (measured, profiles/r02_tune_top.json:
+                // an xy_reuse launch of 8-thread workgroups, U = 8 -> 2: 170 -> 88 ms)
+                const double staging = (double)std::min<int64_t>(4, act * G);
+                const double score = chains * 64.0 + staging * 8.0 + (overlap ? 16.0 : 0.0) + U * 2.0;
                 if (score > best) { best = score; bu = U; bs = (int)G; }
             }
         }
