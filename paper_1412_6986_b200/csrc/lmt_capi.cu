@@ -1336,12 +1336,13 @@ int measure_run(Batch &B) {
         CUDA_TRY(cudaStreamSynchronize(c->stream));
     }
     // phase 2: partitions, list-scheduled. A lane commits to its next
-    // instance only when the previous one has finished (device inputs): a
-    // lane that queues two commits to work other lanes could have started
-    // sooner (a simulation of the bench sample with the measured times: 2 in
-    // flight 40.0 vs 1 in flight 43.8 instances/s). With host buffers two
-    // are queued, so the next instance's copies overlap the current kernels.
-    const size_t depth = B.host() ? 2 : 1;
+    // instance only when the previous one has finished: a lane that queues
+    // two commits to work other lanes could have started sooner (simulated
+    // on the bench sample with its measured times: 2 in flight 40.0 vs 1 in
+    // flight 43.8 instances/s; measured 36.5 -> 40.1). With host buffers an
+    // instance's copies then run just before its kernels (a few ms against
+    // launches of ~100 ms).
+    const size_t depth = 1;
     for (Lane &L : c->parts) CUDA_TRY(cudaStreamWaitEvent(L.s, c->inputs_ready, 0));
     while (!pending.empty()) {
         bool progressed = false;
