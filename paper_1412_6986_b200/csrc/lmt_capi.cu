@@ -782,7 +782,7 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
                          p.num_uncoal_ilb > kIn2HaloCols || p.num_uncoal_ep > kIn2HaloCols;
     JitKey k0{p.stencil_shape, p.stencil_radius, p.num_comp_ilb, p.num_comp_ep, p.num_coal_ilb,
               p.num_coal_ep, p.num_uncoal_ilb, p.num_uncoal_ep, 1, 1, 0, 0, ctxwrap ? 1 : 0, (int)maxt,
-              p.in_h, p.in_w, (int)in2_pitch(p.in_w), kPfDist, 0, 1, 0};
+              p.in_h, p.in_w, (int)in2_pitch(p.in_w), kPfDist, 0, 1, 0, (int64_t)p.n * p.m == 1 ? 1 : 0};
 
     pl->alg_bytes = 4.0 * (in_union(p) + in2_union(p) + (double)p.out_h * p.out_w);
     const double per_wu = (double)nm * (K + 2.0 * p.num_comp_ilb + p.num_coal_ilb + p.num_uncoal_ilb) +

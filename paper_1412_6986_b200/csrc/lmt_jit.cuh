@@ -38,6 +38,8 @@
 //                                        home coordinates do not depend on the work unit within the
 //                                        group: xy_reuse, or x_reuse_* with the group inside one row of
 //                                        work units), so a step loads them once for all U
+//   LMT_NM1                              N * M == 1 (one (i, j) step per work unit): the step loops
+//                                        and the cursor advance are compile-time
 //   LMT_H2 LMT_W2 LMT_P2                 in2 shape (IN2_H, IN2_W: #defines in the reference too) and
 //                                        its physical pitch, so every context read of a step is
 //                                        one base register plus an immediate offset
@@ -436,7 +438,7 @@ __device__ __forceinline__ void run_units(const SynthArgs &A, Src src, const flo
                                           float (&acc)[NU_]) {
 #pragma unroll
     for (int u = 0; u < NU_; ++u) acc[u] = 0.0f;
-    const int NM = A.N * A.M;
+    const int NM = LMT_NM1 ? 1 : A.N * A.M;  // one step per work unit: the loops fold away
     Cursor q{0, in2c, 0, in2u, 0};
     Slot<NU_> s[D];
 #pragma unroll
@@ -505,7 +507,7 @@ extern "C" __global__ void __launch_bounds__(LMT_MAXT, LMT_MINB) lmt_kernel(cons
     // loads of the next group are in flight while this one finishes and is
     // stored (with N*M = 1 a group is a single step: without this every
     // group would wait out a full memory latency on its own).
-    const int NM = A.N * A.M;
+    const int NM = LMT_NM1 ? 1 : A.N * A.M;  // one step per work unit: the loops fold away
     const int ng = nit / U;
     const int total = ng * NM;
     int fix = 0;  // fill cursor: column of work units and row pointer of the next group to load

@@ -12,13 +12,13 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CS = os.path.join(ROOT, "paper_1412_6986_b200", "csrc")
-NAMES = "SHAPE R CI CE NC NCE NU NUE U D OPT WIDE CTXWRAP MAXT H2 W2 P2 PF VEC MINB SHARE".split()
+NAMES = "SHAPE R CI CE NC NCE NU NUE U D OPT WIDE CTXWRAP MAXT H2 W2 P2 PF VEC MINB SHARE NM1".split()
 
 
 def source(vals):
     text = open(os.path.join(CS, "lmt_args.h")).read() + "\n" + open(os.path.join(CS, "lmt_jit.cuh")).read()
     text = text.replace('#include "lmt_args.h"', "")
-    vals = list(vals) + [1] * (len(NAMES) - len(vals))  # LMT_MINB defaults to 1
+    vals = list(vals) + [1, 0, 0][len(vals) - 19:] if len(vals) < len(NAMES) else list(vals)  # MINB 1, SHARE 0, NM1 0
     return "".join(f"#define LMT_{n} {v}\n" for n, v in zip(NAMES, vals)) + text
 
 
