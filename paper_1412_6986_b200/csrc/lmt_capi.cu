@@ -591,9 +591,11 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
         while (bu > 1 && rps(bu) * stage_bytes > smem_cap) bu >>= 1;  // one group's regions must fit
         int64_t G = std::min<int64_t>(4, ngroups(bu));
         while (G > 1 && G * rps(bu) * stage_bytes > smem_cap) G--;
+        // ... leaving at least 48 registers per thread (32 spill the U = 4 group body)
         const int64_t res = std::min<int64_t>({64 / std::max<int64_t>(1, warps), 32,
                                                (228 * 1024) / (G * rps(bu) * stage_bytes + 1024),
-                                               std::max<int64_t>(1, ctas / std::max<int64_t>(1, sms))});
+                                               std::max<int64_t>(1, ctas / std::max<int64_t>(1, sms)),
+                                               65536 / (48 * 32 * std::max<int64_t>(1, warps))});
         if (minb_out) *minb_out = (int)std::max<int64_t>(1, res);
         *U_out = bu;
         *D_out = bd;

@@ -347,11 +347,11 @@ __device__ __forceinline__ void rk_wait(unsigned long long *b, unsigned parity) 
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "RK_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@P1 bra RK_DONE;\n\t"
         "bra RK_WAIT;\n"
         "RK_DONE:\n\t}" ::"r"(rk_smem(b)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 __device__ __forceinline__ void rk_tma2d(void *dst, const RealTmap *m, unsigned long long *bar, int x, int y) {
