@@ -352,9 +352,9 @@ int get_ctx(DevCtx **out) {
         CUDA_TRY(cudaEventCreateWithFlags(&c.inputs_ready, cudaEventDisableTiming));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_rf_mean),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_bulk<16>),
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_tma<16>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_bulk<32>),
+        CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt1_tma<32>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma<16>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
@@ -1738,8 +1738,8 @@ std::string real_violations(const lmt_real_instance &r) {
             return "";
         case 3:
             if (wy != 1 || n % wx || T < 1 || n % T) return "MVT needs wg_y == 1, wg_x | n, tile | n";
-            if (wx % 32 || wx > 512 || (T != 16 && T != 32) || n % 4)
-                return "MVT needs wg_x a multiple of 32 (<= 512), tile 16 or 32, n % 4 == 0";
+            if (wx % 32 || wx > 512 || (T != 16 && T != 32) || n % 256)
+                return "MVT needs wg_x a multiple of 32 (<= 512), tile 16 or 32, n % 256 == 0";
             return "";
         default:
             return "unknown real kernel";
@@ -1824,27 +1824,40 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                 // y is staged whole in shared memory after each kernel's ring
                 const int64_t stage = (int64_t)wx * T * 4, cap = smem_optin - 2048 - (int64_t)n * 4;
                 const int S = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage, (int64_t)n / T});
-                // kernel 1: stages of up to 256 columns (row segments padded by 16 bytes), two when they fit
-                int SC = kMvtStageCols;
-                while (SC > T && ((int64_t)wx * (SC + 4) * 4 * 2 > cap || n % SC)) SC >>= 1;
-                const int64_t stage1 = (int64_t)wx * (SC + 4) * 4;
-                const int S1 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage1, (int64_t)n / SC});
-                if (S < 1 || S1 < 1)
-                    return fail(LMT_ERR_TOO_LARGE, "MVT stages need %lld bytes of shared memory", (long long)stage1);
-                CUtensorMap m2;
+                // kernel 1: stages of NB boxes of bwu + 4 columns (2 x 128 when two stages fit,
+                // else one box, then narrower ones for wide workgroups)
+                int bwu = kMvtBoxCols, NB = kMvtStageCols / kMvtBoxCols;
+                auto st1 = [&]() { return (int64_t)wx * (bwu + 4) * 4 * NB; };
+                while (st1() * 2 > cap && (NB > 1 || bwu > T)) {
+                    if (NB > 1) NB--;
+                    else bwu >>= 1;
+                }
+                const int64_t stage1 = st1();
+                const int S1 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage1, (int64_t)n / (NB * bwu)});
+                if (S < 1 || S1 < 1 || n % (NB * bwu))
+                    return fail(LMT_ERR_TOO_LARGE, "MVT needs n %% %d == 0 and %lld bytes of shared memory per stage",
+                                NB * bwu, (long long)stage1);
+                CUtensorMap m1, m2;
                 const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
                 const cuuint64_t strides[1] = {(cuuint64_t)n * 4};
                 const cuuint32_t estr[2] = {1, 1};
+                const cuuint32_t box1[2] = {(cuuint32_t)(bwu + 4), (cuuint32_t)std::min(wx, 256)};
                 const cuuint32_t box2[2] = {(cuuint32_t)std::min(wx, 256), (cuuint32_t)T};
+                const CUresult e1 = g_encode(&m1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(in[0]), dims,
+                                             strides, box1, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 const CUresult e2 = g_encode(&m2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(in[0]), dims,
                                              strides, box2, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-                if (e2 != CUDA_SUCCESS) return fail(LMT_ERR_CUDA, "MVT tensor map: %d", (int)e2);
+                if (e1 != CUDA_SUCCESS || e2 != CUDA_SUCCESS)
+                    return fail(LMT_ERR_CUDA, "MVT tensor maps: %d %d", (int)e1, (int)e2);
+                const RealTmap t1 = *reinterpret_cast<const RealTmap *>(&m1);
                 const RealTmap t2 = *reinterpret_cast<const RealTmap *>(&m2);
                 const size_t ybytes = (size_t)n * 4;
-                if (T == 32) k_mvt1_bulk<32><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(in[0], in[1], in[3], out, n, S1, SC);
-                else k_mvt1_bulk<16><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(in[0], in[1], in[3], out, n, S1, SC);
+                if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwu, NB);
+                else k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwu, NB);
                 CUDA_TRY(cudaGetLastError());
                 if (T == 32) k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
                 else k_mvt2_tma<16><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);

@@ -394,36 +394,36 @@ __device__ __forceinline__ void rk_stage_vec(float *dst, const float *src, int n
     }
 }
 
-__device__ __forceinline__ void rk_bulk(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     rk_smem(dst)),
-                 "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(rk_smem(bar))
-                 : "memory");
-}
-
-// Kernel 1 (row dots): a ring of S stages, each SC columns (256, fewer for
-// wide workgroups) of the CTA's wg rows, one 1D bulk copy (cp.async.bulk,
-// the TMA engine) per row segment -- 1 KB requests instead of the 128-byte
-// rows of a 2D box -- into rows padded by 16 bytes, so a quarter-warp's
-// 128-bit reads of 8 rows hit 8 distinct bank groups. Warp 0 issues the
-// copies (expect_tx first, then one row per lane) and refills a stage once
-// every warp released it. Kernel 2 (column dots): stages of T rows x wg
-// columns by 2D TMA boxes, read one float per lane (consecutive). Each
-// thread's registers hold the next sub-step (kernel 1) / stage (kernel 2)
-// while the current FMAs run: one warp per SM carries the serial chains, so
-// latency is the limit.
-constexpr int kMvtStageCols = 256;
+// Kernel 1 (row dots): a ring of S stages, each 256 columns of the CTA's wg
+// rows as two 2D TMA boxes of 128 + 4 columns: the 4 extra columns (3 %
+// more bytes; zero-filled past the matrix) make the staged row pitch 528
+// bytes = 33 x 16, so a quarter-warp's 128-bit reads of 8 rows hit 8
+// distinct bank groups without swizzling, and each box row is a 528-byte
+// request (2D boxes with the 128B swizzle are limited to 128-byte rows;
+// one cp.async.bulk per row costs one issue per row in the only warp).
+// Kernel 2 (column dots): stages of T rows x wg columns by 2D TMA boxes,
+// read one float per lane (consecutive). Thread 0 issues the loads and
+// refills a stage once every warp released it; each thread's registers hold
+// the next sub-step while the current FMAs run: one warp per SM carries the
+// serial chains, so latency is the limit.
+constexpr int kMvtBoxCols = 128;  // useful columns per box (+4 padding columns)
+constexpr int kMvtStageCols = 2 * kMvtBoxCols;
 template <int T>
-__global__ void __launch_bounds__(512) k_mvt1_bulk(const float *__restrict__ A, const float *__restrict__ y1,
-                                                   const float *__restrict__ x1_0, float *__restrict__ x1, int n,
-                                                   int S, int SC) {
+__global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y1,
+                                                  const float *__restrict__ x1_0, float *__restrict__ x1, int n,
+                                                  int S, int bwu, int NB) {
+    // NB boxes of bwu useful columns per stage (2 x 128; fewer / narrower for wide workgroups)
+    const int BW = bwu + 4;        // floats per staged row of a box: pitch = 16 x odd bytes
+    const int SC = NB * bwu;       // columns per stage
+    const int KB = SC / T;         // sub-steps per stage
     extern __shared__ unsigned char rk_raw[];
     __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
     float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
-    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int i0 = blockIdx.x * wg, steps = n / SC, KB = SC / T;
-    const int pitch = SC + 4;        // floats per staged row (+16 bytes: rows rotate through the bank groups)
-    const int sf = wg * pitch;       // floats per stage
+    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int i0 = blockIdx.x * wg, steps = n / SC;
+    const int boxes = (wg + 255) / 256, brows = wg < 256 ? wg : 256;
+    const int bf = wg * BW;       // floats per box (all rows)
+    const int sf = NB * bf;       // floats per stage
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             rk_bar_init(&full[s], 1);
@@ -432,25 +432,23 @@ __global__ void __launch_bounds__(512) k_mvt1_bulk(const float *__restrict__ A, 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // warp 0 only: lane 0 arms the barrier for the stage's bytes, then every
-    // lane copies its rows
     auto issue = [&](int slot, int step) {
-        if (lane == 0) rk_expect(&full[slot], (unsigned)(wg * SC * 4));
-        __syncwarp();
-        for (int r = lane; r < wg; r += 32)
-            rk_bulk(st + slot * sf + r * pitch, A + (size_t)(i0 + r) * n + (size_t)step * SC, (unsigned)(SC * 4),
-                    &full[slot]);
+        rk_expect(&full[slot], (unsigned)(sf * 4));
+        for (int nb = 0; nb < NB; ++nb)
+            for (int b = 0; b < boxes; ++b)
+                rk_tma2d(st + slot * sf + nb * bf + b * 256 * BW, &tm, &full[slot], step * SC + nb * bwu,
+                         i0 + b * brows);
     };
-    if (warp == 0)
+    if (tid == 0)
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
     float *ys = st + (size_t)S * sf;  // y, whole, after the ring: LDS broadcasts
     rk_stage_vec(ys, y1, n, tid, wg);
     __syncthreads();
     const unsigned ybase = rk_smem(ys);
     float acc = x1_0[i0 + tid];
-    const unsigned base = rk_smem(st) + (unsigned)(tid * pitch * 4);
+    const unsigned base = rk_smem(st) + (unsigned)(tid * BW * 4);
     // two register buffers, ping-pong: sub-step k = (stage k / KB, T-column
-    // slice k % KB) computes from one while the other receives k + 1
+    // slice kb = k % KB) computes from one while the other receives k + 1
     float4 a0[T / 4], a1[T / 4];
     const int total = steps * KB;
     int slot = 0, kb = 0, step = 0;
@@ -464,10 +462,11 @@ __global__ void __launch_bounds__(512) k_mvt1_bulk(const float *__restrict__ A, 
         nph ^= 1;                     \
     }                                 \
     const int nkb = last ? 0 : kb + 1;
-#define MVT1_LOAD(A_, sl, bk)                                                          \
-    {                                                                                  \
-        const unsigned bx = base + (unsigned)(((sl) * sf + (bk) * T) * 4);             \
-        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) A_[c] = rk_lds4(bx + (unsigned)(c << 4)); \
+#define MVT1_LOAD(A_, sl, bk)                                                                                   \
+    {                                                                                                           \
+        const int col = (bk) * T;                                                                               \
+        const unsigned bx = base + (unsigned)(((sl) * sf + (col / bwu) * bf + (col % bwu)) * 4);              \
+        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) A_[c] = rk_lds4(bx + (unsigned)(c << 4));            \
     }
 #define MVT1_FMA(A_, kk)                                                       \
     _Pragma("unroll") for (int c = 0; c < T / 4; ++c) {                        \
@@ -477,16 +476,15 @@ __global__ void __launch_bounds__(512) k_mvt1_bulk(const float *__restrict__ A, 
         acc = __fmaf_rn(A_[c].z, yv.z, acc);                                   \
         acc = __fmaf_rn(A_[c].w, yv.w, acc);                                   \
     }
-#define MVT1_RELEASE(last)                                \
-    if (last) {                                           \
-        __syncwarp();                                     \
-        if (lane == 0) rk_arrive(&empty[slot]);           \
-        if (warp == 0 && step + S < steps) {              \
-            if (lane == 0) rk_wait(&empty[slot], phase);  \
-            __syncwarp();                                 \
-            issue(slot, step + S);                        \
-        }                                                 \
-        ++step;                                           \
+#define MVT1_RELEASE(last)                      \
+    if (last) {                                 \
+        __syncwarp();                           \
+        if (lane == 0) rk_arrive(&empty[slot]); \
+        if (tid == 0 && step + S < steps) {     \
+            rk_wait(&empty[slot], phase);       \
+            issue(slot, step + S);              \
+        }                                       \
+        ++step;                                 \
     }
     rk_wait(&full[0], 0);
     MVT1_LOAD(a0, 0, 0)
@@ -555,49 +553,50 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
     rk_stage_vec(ysm, y2, n, tid, wg);
     __syncthreads();
     const unsigned ybase = rk_smem(ysm);
-    float ca[T], na[T];
-    float4 cy[T / 4], ny[T / 4];
-    auto load = [&](float (&a)[T], float4 (&y)[T / 4], int slot, int step) {
-#pragma unroll
-        for (int jj = 0; jj < T; ++jj) a[jj] = rk_lds(base + (unsigned)((slot * sf + jj * bcols) * 4));
-#pragma unroll
-        for (int q = 0; q < T / 4; ++q) y[q] = rk_lds4(ybase + (unsigned)((step * T + 4 * q) * 4));
-    };
-    rk_wait(&full[0], 0);
-    load(ca, cy, 0, 0);
+    float a0[T], a1[T];
     int slot = 0;
     unsigned phase = 0;
-    for (int step = 0; step < steps; ++step) {
-        int ns = slot + 1;
-        unsigned nph = phase;
-        if (ns == S) {
-            ns = 0;
-            nph ^= 1;
-        }
-        if (step + 1 < steps) {
-            rk_wait(&full[ns], nph);
-            load(na, ny, ns, step + 1);
-        }
-#pragma unroll
-        for (int q = 0; q < T / 4; ++q) {
-            acc = __fmaf_rn(ca[4 * q + 0], cy[q].x, acc);
-            acc = __fmaf_rn(ca[4 * q + 1], cy[q].y, acc);
-            acc = __fmaf_rn(ca[4 * q + 2], cy[q].z, acc);
-            acc = __fmaf_rn(ca[4 * q + 3], cy[q].w, acc);
-        }
-        __syncwarp();
-        if (lane == 0) rk_arrive(&empty[slot]);
-        if (tid == 0 && step + S < steps) {
-            rk_wait(&empty[slot], phase);
-            issue(slot, step + S);
-        }
-#pragma unroll
-        for (int jj = 0; jj < T; ++jj) ca[jj] = na[jj];
-#pragma unroll
-        for (int q = 0; q < T / 4; ++q) cy[q] = ny[q];
-        slot = ns;
-        phase = nph;
+#define MVT2_LOAD(A_, sl)                                                                                    \
+    _Pragma("unroll") for (int jj = 0; jj < T; ++jj) A_[jj] = rk_lds(base + (unsigned)(((sl) * sf + jj * bcols) * 4));
+#define MVT2_FMA(A_, stp)                                                                      \
+    _Pragma("unroll") for (int q = 0; q < T / 4; ++q) {                                        \
+        const float4 yv = rk_lds4(ybase + (unsigned)(((stp) * T + 4 * q) * 4));               \
+        acc = __fmaf_rn(A_[4 * q + 0], yv.x, acc);                                             \
+        acc = __fmaf_rn(A_[4 * q + 1], yv.y, acc);                                             \
+        acc = __fmaf_rn(A_[4 * q + 2], yv.z, acc);                                             \
+        acc = __fmaf_rn(A_[4 * q + 3], yv.w, acc);                                             \
     }
+#define MVT2_STEP(CUR, NXT, stp)                         \
+    {                                                    \
+        int ns = slot + 1;                               \
+        unsigned nph = phase;                            \
+        if (ns == S) {                                   \
+            ns = 0;                                      \
+            nph ^= 1;                                    \
+        }                                                \
+        if ((stp) + 1 < steps) {                         \
+            rk_wait(&full[ns], nph);                     \
+            MVT2_LOAD(NXT, ns)                           \
+        }                                                \
+        MVT2_FMA(CUR, stp)                               \
+        __syncwarp();                                    \
+        if (lane == 0) rk_arrive(&empty[slot]);          \
+        if (tid == 0 && (stp) + S < steps) {             \
+            rk_wait(&empty[slot], phase);                \
+            issue(slot, (stp) + S);                      \
+        }                                                \
+        slot = ns;                                       \
+        phase = nph;                                     \
+    }
+    rk_wait(&full[0], 0);
+    MVT2_LOAD(a0, 0)
+    for (int step = 0; step < steps; step += 2) {
+        MVT2_STEP(a0, a1, step)
+        if (step + 1 < steps) MVT2_STEP(a1, a0, step + 1)
+    }
+#undef MVT2_LOAD
+#undef MVT2_FMA
+#undef MVT2_STEP
     x2[i0 + tid] = acc;
 }
 
