@@ -1828,7 +1828,7 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                 // else one box, then narrower ones for wide workgroups)
                 int bwu = kMvtBoxCols, NB = kMvtStageCols / kMvtBoxCols;
                 auto st1 = [&]() { return (int64_t)wx * (bwu + 4) * 4 * NB; };
-                while (st1() * 2 > cap && (NB > 1 || bwu > T)) {
+                while (st1() * 2 > cap && (NB > 1 || bwu > 16)) {
                     if (NB > 1) NB--;
                     else bwu >>= 1;
                 }
@@ -1855,12 +1855,31 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                     return fail(LMT_ERR_CUDA, "MVT tensor maps: %d %d", (int)e1, (int)e2);
                 const RealTmap t1 = *reinterpret_cast<const RealTmap *>(&m1);
                 const RealTmap t2 = *reinterpret_cast<const RealTmap *>(&m2);
+                // kernel 2 with 16-row stages (T = 16, or wide workgroups of T = 32)
+                const int64_t stage16 = (int64_t)wx * 16 * 4;
+                const int S16 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage16, (int64_t)n / 16});
+                RealTmap t2x = t2;
+                if (T == 32 && wx > 256) {
+                    CUtensorMap m3;
+                    const cuuint32_t box3[2] = {(cuuint32_t)std::min(wx, 256), 16u};
+                    if (g_encode(&m3, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(in[0]), dims, strides, box3,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                        return fail(LMT_ERR_CUDA, "MVT tensor map");
+                    t2x = *reinterpret_cast<const RealTmap *>(&m3);
+                }
                 const size_t ybytes = (size_t)n * 4;
-                if (T == 32) k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwu, NB);
-                else k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwu, NB);
+                int bwl = 0;
+                while ((1 << bwl) < bwu) bwl++;
+                if (T == 32 && wx <= 256 && bwu >= 32)
+                    k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwl, NB);
+                else
+                    k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwl, NB);
                 CUDA_TRY(cudaGetLastError());
-                if (T == 32) k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
-                else k_mvt2_tma<16><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
+                if (T == 32 && wx <= 256)
+                    k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
+                else  // T = 16 stages (same results: T only sets the staging granularity)
+                    k_mvt2_tma<16><<<grd, wx, (size_t)S16 * stage16 + 128 + ybytes, s>>>(t2x, in[2], in[4], out + n, n, S16);
             }
             break;
         }

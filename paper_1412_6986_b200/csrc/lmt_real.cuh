@@ -408,10 +408,17 @@ __device__ __forceinline__ void rk_stage_vec(float *dst, const float *src, int n
 // serial chains, so latency is the limit.
 constexpr int kMvtBoxCols = 128;  // useful columns per box (+4 padding columns)
 constexpr int kMvtStageCols = 2 * kMvtBoxCols;
+// (T = 32 needs ~150 registers for its two buffers of row values and y:
+// launch bounds of 256 threads; wider workgroups use the T = 16 kernel, whose
+// results are the same -- T only sets the staging granularity, the chain is
+// j ascending either way)
 template <int T>
-__global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y1,
-                                                  const float *__restrict__ x1_0, float *__restrict__ x1, int n,
-                                                  int S, int bwu, int NB) {
+__global__ void __launch_bounds__(T == 32 ? 256 : 512) k_mvt1_tma(const __grid_constant__ RealTmap tm,
+                                                                 const float *__restrict__ y1,
+                                                                 const float *__restrict__ x1_0,
+                                                                 float *__restrict__ x1, int n, int S, int bwl,
+                                                                 int NB) {
+    const int bwu = 1 << bwl;
     // NB boxes of bwu useful columns per stage (2 x 128; fewer / narrower for wide workgroups)
     const int BW = bwu + 4;        // floats per staged row of a box: pitch = 16 x odd bytes
     const int SC = NB * bwu;       // columns per stage
@@ -449,7 +456,7 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
     const unsigned base = rk_smem(st) + (unsigned)(tid * BW * 4);
     // two register buffers, ping-pong: sub-step k = (stage k / KB, T-column
     // slice kb = k % KB) computes from one while the other receives k + 1
-    float4 a0[T / 4], a1[T / 4];
+    float4 a0[T / 4], a1[T / 4], y0[T / 4], y1v[T / 4];
     const int total = steps * KB;
     int slot = 0, kb = 0, step = 0;
     unsigned phase = 0;
@@ -462,19 +469,21 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
         nph ^= 1;                     \
     }                                 \
     const int nkb = last ? 0 : kb + 1;
-#define MVT1_LOAD(A_, sl, bk)                                                                                   \
-    {                                                                                                           \
-        const int col = (bk) * T;                                                                               \
-        const unsigned bx = base + (unsigned)(((sl) * sf + (col / bwu) * bf + (col % bwu)) * 4);              \
-        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) A_[c] = rk_lds4(bx + (unsigned)(c << 4));            \
+#define MVT1_LOAD(A_, Y_, sl, bk, kk)                                                                  \
+    {                                                                                                  \
+        const int col = (bk) * T;                                                                      \
+        const unsigned bx = base + (unsigned)(((sl) * sf + (col >> bwl) * bf + (col & (bwu - 1))) * 4); \
+        _Pragma("unroll") for (int c = 0; c < T / 4; ++c) {                                           \
+            A_[c] = rk_lds4(bx + (unsigned)(c << 4));                                                  \
+            Y_[c] = rk_lds4(ybase + (unsigned)(((kk) * T + 4 * c) * 4));                               \
+        }                                                                                              \
     }
-#define MVT1_FMA(A_, kk)                                                       \
-    _Pragma("unroll") for (int c = 0; c < T / 4; ++c) {                        \
-        const float4 yv = rk_lds4(ybase + (unsigned)(((kk) * T + 4 * c) * 4)); \
-        acc = __fmaf_rn(A_[c].x, yv.x, acc);                                   \
-        acc = __fmaf_rn(A_[c].y, yv.y, acc);                                   \
-        acc = __fmaf_rn(A_[c].z, yv.z, acc);                                   \
-        acc = __fmaf_rn(A_[c].w, yv.w, acc);                                   \
+#define MVT1_FMA(A_, Y_)                                    \
+    _Pragma("unroll") for (int c = 0; c < T / 4; ++c) {     \
+        acc = __fmaf_rn(A_[c].x, Y_[c].x, acc);             \
+        acc = __fmaf_rn(A_[c].y, Y_[c].y, acc);             \
+        acc = __fmaf_rn(A_[c].z, Y_[c].z, acc);             \
+        acc = __fmaf_rn(A_[c].w, Y_[c].w, acc);             \
     }
 #define MVT1_RELEASE(last)                      \
     if (last) {                                 \
@@ -487,15 +496,15 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
         ++step;                                 \
     }
     rk_wait(&full[0], 0);
-    MVT1_LOAD(a0, 0, 0)
+    MVT1_LOAD(a0, y0, 0, 0, 0)
     for (int k = 0; k < total; k += 2) {
         {  // sub-step k from buffer 0, k + 1 into buffer 1
             MVT1_NEXT(ns, nph, nkb, last)
             if (k + 1 < total) {
                 if (last) rk_wait(&full[ns], nph);
-                MVT1_LOAD(a1, ns, nkb)
+                MVT1_LOAD(a1, y1v, ns, nkb, k + 1)
             }
-            MVT1_FMA(a0, k)
+            MVT1_FMA(a0, y0)
             MVT1_RELEASE(last)
             slot = ns;
             phase = nph;
@@ -505,9 +514,9 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
             MVT1_NEXT(ns, nph, nkb, last)
             if (k + 2 < total) {
                 if (last) rk_wait(&full[ns], nph);
-                MVT1_LOAD(a0, ns, nkb)
+                MVT1_LOAD(a0, y0, ns, nkb, k + 2)
             }
-            MVT1_FMA(a1, k + 1)
+            MVT1_FMA(a1, y1v)
             MVT1_RELEASE(last)
             slot = ns;
             phase = nph;
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(512) k_mvt1_tma(const __grid_constant__ RealTm
 }
 
 template <int T>
-__global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y2,
+__global__ void __launch_bounds__(T == 32 ? 256 : 512) k_mvt2_tma(const __grid_constant__ RealTmap tm, const float *__restrict__ y2,
                                                   const float *__restrict__ x2_0, float *__restrict__ x2, int n,
                                                   int S) {
     extern __shared__ unsigned char rk_raw[];
@@ -554,19 +563,22 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
     __syncthreads();
     const unsigned ybase = rk_smem(ysm);
     float a0[T], a1[T];
+    float4 y0[T / 4], y1v[T / 4];
     int slot = 0;
     unsigned phase = 0;
-#define MVT2_LOAD(A_, sl)                                                                                    \
-    _Pragma("unroll") for (int jj = 0; jj < T; ++jj) A_[jj] = rk_lds(base + (unsigned)(((sl) * sf + jj * bcols) * 4));
-#define MVT2_FMA(A_, stp)                                                                      \
-    _Pragma("unroll") for (int q = 0; q < T / 4; ++q) {                                        \
-        const float4 yv = rk_lds4(ybase + (unsigned)(((stp) * T + 4 * q) * 4));               \
-        acc = __fmaf_rn(A_[4 * q + 0], yv.x, acc);                                             \
-        acc = __fmaf_rn(A_[4 * q + 1], yv.y, acc);                                             \
-        acc = __fmaf_rn(A_[4 * q + 2], yv.z, acc);                                             \
-        acc = __fmaf_rn(A_[4 * q + 3], yv.w, acc);                                             \
+#define MVT2_LOAD(A_, Y_, sl, stp)                                                                            \
+    {                                                                                                         \
+        _Pragma("unroll") for (int jj = 0; jj < T; ++jj) A_[jj] = rk_lds(base + (unsigned)(((sl) * sf + jj * bcols) * 4)); \
+        _Pragma("unroll") for (int q = 0; q < T / 4; ++q) Y_[q] = rk_lds4(ybase + (unsigned)(((stp) * T + 4 * q) * 4)); \
     }
-#define MVT2_STEP(CUR, NXT, stp)                         \
+#define MVT2_FMA(A_, Y_)                                      \
+    _Pragma("unroll") for (int q = 0; q < T / 4; ++q) {       \
+        acc = __fmaf_rn(A_[4 * q + 0], Y_[q].x, acc);         \
+        acc = __fmaf_rn(A_[4 * q + 1], Y_[q].y, acc);         \
+        acc = __fmaf_rn(A_[4 * q + 2], Y_[q].z, acc);         \
+        acc = __fmaf_rn(A_[4 * q + 3], Y_[q].w, acc);         \
+    }
+#define MVT2_STEP(CUR, CY, NXT, NY, stp)                 \
     {                                                    \
         int ns = slot + 1;                               \
         unsigned nph = phase;                            \
@@ -576,9 +588,9 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
         }                                                \
         if ((stp) + 1 < steps) {                         \
             rk_wait(&full[ns], nph);                     \
-            MVT2_LOAD(NXT, ns)                           \
+            MVT2_LOAD(NXT, NY, ns, (stp) + 1)            \
         }                                                \
-        MVT2_FMA(CUR, stp)                               \
+        MVT2_FMA(CUR, CY)                                \
         __syncwarp();                                    \
         if (lane == 0) rk_arrive(&empty[slot]);          \
         if (tid == 0 && (stp) + S < steps) {             \
@@ -589,10 +601,10 @@ __global__ void __launch_bounds__(512) k_mvt2_tma(const __grid_constant__ RealTm
         phase = nph;                                     \
     }
     rk_wait(&full[0], 0);
-    MVT2_LOAD(a0, 0)
+    MVT2_LOAD(a0, y0, 0, 0)
     for (int step = 0; step < steps; step += 2) {
-        MVT2_STEP(a0, a1, step)
-        if (step + 1 < steps) MVT2_STEP(a1, a0, step + 1)
+        MVT2_STEP(a0, y0, a1, y1v, step)
+        if (step + 1 < steps) MVT2_STEP(a1, y1v, a0, y0, step + 1)
     }
 #undef MVT2_LOAD
 #undef MVT2_FMA
