@@ -481,7 +481,13 @@ def run_ours(args, rank: int, world: int, local_rank: int, meta_group):
         line["e2e"] = e2e
     if hbm:
         line["hbm_leg"] = hbm
-        line["roofline"]["traffic"] = hbm.get("traffic")
+        tr = hbm.get("traffic") or {}
+        if "baseline" in tr:  # ncu DRAM bytes of one lmt_kernel launch (the 8192^2 HBM leg), per launch
+            line["roofline"]["traffic"] = tr["baseline"]["dram_bytes_per_launch"]
+            line["roofline"]["traffic_note"] = (
+                f"dram__bytes_read+write of one K1 launch of the 8192^2 star leg: {tr['baseline']['dram_bytes_per_launch']:.4g}"
+                f" B vs {tr['algorithmic_bytes_per_launch']:.4g} algorithmic (K2: "
+                f"{tr['optimized']['dram_bytes_per_launch']:.4g}); profiles/r02_hbm_traffic.json")
     if rf:
         line["rf"] = rf
     if real:

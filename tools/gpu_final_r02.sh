@@ -15,9 +15,10 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 2400 python bench.py --dump $OUT/bench_sample.npz > $OUT/bench.json 2> $OUT/bench.err; echo "rc=$?" >> $OUT/bench.err
 timeout 900 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 1 --warmup 1 --batch 96 --no-e2e --no-cpu --no-rf --no-real --no-hbm > $OUT/ncu_bench.log 2>&1
+    python bench.py --steps 1 --warmup 1 --batch 96 --isolated --no-e2e --no-cpu --no-rf --no-real --no-hbm > $OUT/ncu_bench.log 2>&1
 gzip -f $OUT/launches.csv
 bash tools/ncu_hbm.sh ${TAG}_hbm > /dev/null 2>&1
+bash tools/ncu_src.sh ${TAG}_H16 2048,2048,8192,8192,5,1,1,2,1,0,0,0,0,0,0,2048,2048,32,8 > /dev/null 2>&1
 E=2048,2048,1024,1024,0,64,64,2,1,6,44,13,0,2,4,256,1024,2,1
 python tools/ncu_one.py $E > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:lmt_kernel -c 2 \
