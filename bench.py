@@ -53,9 +53,11 @@ CFG1 = (1024, 1024, 1024, 1024, 5, 1, 1, 2, 1, 0, 0, 0, 0, 0, 0, 1024, 1024, 16,
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256, help="instances per rank per step")
+    ap.add_argument("--batch", type=int, default=1024,
+                    help="instances per rank per step: the batch the measurement engine schedules at once "
+                         "(run_sweep's checkpoint chunk)")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--samples", type=int, default=32, help="output cells per instance checked against the oracle")

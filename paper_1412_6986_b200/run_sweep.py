@@ -34,7 +34,8 @@ def _args(argv=None):
     ap.add_argument("--out", required=True)
     ap.add_argument("--max-instances", type=int, default=1_000_000)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--chunk", type=int, default=256, help="instances per checkpoint")
+    ap.add_argument("--chunk", type=int, default=1024,
+                    help="instances per checkpoint, measured as one batch (small launches packed into SM partitions)")
     ap.add_argument("--limit", type=int, default=0, help="only the first N rows of this rank's share (testing)")
     ap.add_argument("--sample", type=int, default=0, help="a seeded random subset of N rows of the selection")
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl with a GPU, else gloo)")
@@ -43,8 +44,10 @@ def _args(argv=None):
     ap.add_argument("--family", default="all", choices=("all", "dla", "grid"),
                     help="restrict to the dense-linear-algebra or structured-grid patterns (sweep.DLA_FAMILY / "
                          "GRID_FAMILY)")
-    ap.add_argument("--concurrent", action="store_true",
-                    help="launches of <= 74 CTAs in disjoint SM partitions (the bench's placement)")
+    ap.add_argument("--concurrent", action="store_true", default=True,
+                    help="launches of <= 74 CTAs in disjoint SM partitions (the default: the bench's placement)")
+    ap.add_argument("--isolated", dest="concurrent", action="store_false",
+                    help="every launch alone on the whole device")
     ap.add_argument("--regblock", action="store_true",
                     help="register-blocked variants (units sharing home coordinates load once) instead of the "
                          "literal ones (DESIGN.md 5, the measurement contract)")
