@@ -1727,9 +1727,11 @@ std::string real_violations(const lmt_real_instance &r) {
                        "tile | n";
             return "";
         case 1:
-            if (T != wx || T > 32 || T % wy || n % T) return "matrixMul needs tile == wg_x <= 32, wg_y | tile, tile | n";
-            if (T / wy != 1 && T / wy != 2 && T / wy != 4 && T / wy != 8) return "matrixMul work per thread tile/wg_y must be 1, 2, 4 or 8";
-            if (T % 4) return "matrixMul tile must be a multiple of 4";
+            if (T > 64 || T % wx || T % wy || n % T || T % 4 || n % 4)
+                return "matrixMul needs tile <= 64, a multiple of 4 dividing n, wg_x | tile, wg_y | tile";
+            if (T / wy != 1 && T / wy != 2 && T / wy != 4 && T / wy != 8) return "matrixMul rows per thread tile/wg_y must be 1, 2, 4 or 8";
+            if (T / wx != 1 && T / wx != 2 && T / wx != 4) return "matrixMul columns per thread tile/wg_x must be 1, 2 or 4";
+            if ((T * T / 4 + wx * wy - 1) / (wx * wy) > 8) return "matrixMul tile copy needs at most 8 float4 per thread";
             return "";
         case 2:
             if (T < 1) return "convolution outputs per thread (tile) must be >= 1";
@@ -1781,14 +1783,24 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
         }
         case 1: {
             const dim3 grd(n / T, n / T);
-            const int W = T / wy;
-            if (variant == 0) { k_matmul_base<<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W); break; }
-            const size_t sm = ((size_t)T * (T + 4) + (size_t)T * T) * 4;
-            if (W == 1) k_matmul_opt<1><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
-            else if (W == 2) k_matmul_opt<2><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
-            else if (W == 4) k_matmul_opt<4><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
-            else k_matmul_opt<8><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);
-            break;
+            const int W = T / wy, CC = T / wx;
+            if (variant == 0) {
+                if (CC == 1) k_matmul_base<1><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
+                else if (CC == 2) k_matmul_base<2><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
+                else k_matmul_base<4><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
+                break;
+            }
+            const size_t sm = (size_t)2 * T * (T + 4) * 4;
+#define LMT_MM(WW, C_)                                                                    \
+    if (W == WW && CC == C_) {                                                            \
+        k_matmul_opt<WW, C_><<<grd, blk, sm, s>>>(in[0], in[1], out, n, T);              \
+        break;                                                                            \
+    }
+            LMT_MM(1, 1) LMT_MM(2, 1) LMT_MM(4, 1) LMT_MM(8, 1)
+            LMT_MM(1, 2) LMT_MM(2, 2) LMT_MM(4, 2) LMT_MM(8, 2)
+            LMT_MM(1, 4) LMT_MM(2, 4) LMT_MM(4, 4) LMT_MM(8, 4)
+#undef LMT_MM
+            return fail(LMT_ERR_INVALID_INSTANCE, "matrixMul shape");
         }
         case 2: {
             const RealConv c = real_weights(r.radius);

@@ -86,84 +86,115 @@ __global__ void k_transpose_opt(const float *__restrict__ A, float *__restrict__
 }
 
 // ------------------------------------------------------------ matrixMul
-// C = A x B, n x n. CTA = T x T outputs, blockDim (T, T / W): thread (tx, ty)
-// computes rows ty + r * (T / W), r < W, column tx. acc = fmaf(A[i][k], B[k][j], acc), k ascending.
+// C = A x B, n x n. CTA = T x T outputs, blockDim (T / CC, T / W): thread
+// (tx, ty) computes rows ty + r * (T / W), r < W, and columns CC * tx + q,
+// q < CC (CC = 1: the SDK form, one column per thread; the tiling factors W
+// and CC are the instance's). acc = fmaf(A[i][k], B[k][j], acc), k ascending.
 // Both variants take k four at a time: one 128-bit read of A[row][k .. k+3]
-// per row (the same address across the warp: a broadcast) feeds 4 FMAs per
-// output, so the W rows' 4W FMAs cost W + 4 loads instead of 2 per FMA.
+// per row (the same address across the lanes of a row: a broadcast) and one
+// CC-wide read of B[k][cols] per k feed 4 * W * CC FMAs, so a thread's
+// register tile costs W + 4 loads per 4 k instead of 2 per FMA.
+template <int CC>
 __global__ void k_matmul_base(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
                               int n, int T, int W) {
+    using V = typename VecOf<CC>::T;
     const int h = T / W;
-    const int col = blockIdx.x * T + threadIdx.x;
+    const int col = blockIdx.x * T + CC * threadIdx.x;
     for (int r = 0; r < W; ++r) {
         const int row = blockIdx.y * T + threadIdx.y + r * h;
         const float *ar = A + (size_t)row * n;
-        float acc = 0.0f;
+        float acc[CC];
+#pragma unroll
+        for (int q = 0; q < CC; ++q) acc[q] = 0.0f;
         if ((n & 3) == 0) {
             for (int k = 0; k < n; k += 4) {
                 const float4 a = __ldg(reinterpret_cast<const float4 *>(ar + k));
-                acc = __fmaf_rn(a.x, __ldg(B + (size_t)(k + 0) * n + col), acc);
-                acc = __fmaf_rn(a.y, __ldg(B + (size_t)(k + 1) * n + col), acc);
-                acc = __fmaf_rn(a.z, __ldg(B + (size_t)(k + 2) * n + col), acc);
-                acc = __fmaf_rn(a.w, __ldg(B + (size_t)(k + 3) * n + col), acc);
+                const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const V bv = __ldg(reinterpret_cast<const V *>(B + (size_t)(k + kk) * n + col));
+#pragma unroll
+                    for (int q = 0; q < CC; ++q) acc[q] = __fmaf_rn(av[kk], vget<CC>(bv, q), acc[q]);
+                }
             }
         } else {
-            for (int k = 0; k < n; ++k) acc = __fmaf_rn(ar[k], B[(size_t)k * n + col], acc);
+            for (int k = 0; k < n; ++k)
+#pragma unroll
+                for (int q = 0; q < CC; ++q) acc[q] = __fmaf_rn(ar[k], B[(size_t)k * n + col + q], acc[q]);
         }
-        C[(size_t)row * n + col] = acc;
+#pragma unroll
+        for (int q = 0; q < CC; ++q) C[(size_t)row * n + col + q] = acc[q];
     }
 }
 
-// optimized: A and B tiles staged in shared memory (As rows padded to T + 4
-// floats: 16-byte aligned for the 128-bit k reads), the next tiles' elements
+// optimized: A and B tiles staged in shared memory (rows padded to T + 4
+// floats: 16-byte aligned for the 128-bit reads), the next tiles' elements
 // loaded into registers while the current tiles are consumed.
-template <int W>
+template <int W, int CC>
 __global__ void k_matmul_opt(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
                              int n, int T) {
-    extern __shared__ __align__(16) float sm[];  // As[T][T + 4], Bs[T][T]
-    const int PA = T + 4, h = T / W;
-    float *As = sm, *Bs = sm + T * PA;
+    using V = typename VecOf<CC>::T;
+    extern __shared__ __align__(16) float sm[];  // As[T][T + 4], Bs[T][T + 4]
+    const int P = T + 4, h = T / W;
+    float *As = sm, *Bs = sm + T * P;
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int col = blockIdx.x * T + tx;
-    const size_t arow0 = (size_t)(blockIdx.y * T) * n;
-    float acc[W], ra[W], rb[W];
+    const int nthr = blockDim.x * blockDim.y, tid = ty * blockDim.x + tx;
+    const int col0 = blockIdx.x * T, row0 = blockIdx.y * T;
+    // tile copy: each thread moves (T * T) / nthr elements of A and of B per
+    // k-tile, four at a time (T % 4 == 0): element e = 4 * (tid + i * nthr)
+    const int per4 = (T * T / 4 + nthr - 1) / nthr;
+    float acc[W][CC];
 #pragma unroll
-    for (int r = 0; r < W; ++r) {
-        acc[r] = 0.0f;
-        ra[r] = A[arow0 + (size_t)(ty + r * h) * n + tx];
-        rb[r] = B[(size_t)(ty + r * h) * n + col];
-    }
+    for (int r = 0; r < W; ++r)
+#pragma unroll
+        for (int q = 0; q < CC; ++q) acc[r][q] = 0.0f;
+    float4 ra[8], rb[8];  // up to 8 float4 per thread per tile (T <= 64, >= 128 threads; T <= 32: >= 32)
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (i < per4) {
+                const int e = 4 * (tid + i * nthr);
+                if (e < T * T) {
+                    const int rr = e / T, cc = e - rr * T;
+                    ra[i] = __ldg(reinterpret_cast<const float4 *>(A + (size_t)(row0 + rr) * n + k0 + cc));
+                    rb[i] = __ldg(reinterpret_cast<const float4 *>(B + (size_t)(k0 + rr) * n + col0 + cc));
+                }
+            }
+    };
+    fetch(0);
     for (int k0 = 0; k0 < n; k0 += T) {
 #pragma unroll
-        for (int r = 0; r < W; ++r) {
-            const int lr = ty + r * h;
-            As[lr * PA + tx] = ra[r];
-            Bs[lr * T + tx] = rb[r];
-        }
-        __syncthreads();
-        if (k0 + T < n) {
-#pragma unroll
-            for (int r = 0; r < W; ++r) {
-                ra[r] = __ldg(A + arow0 + (size_t)(ty + r * h) * n + k0 + T + tx);
-                rb[r] = __ldg(B + (size_t)(k0 + T + ty + r * h) * n + col);
+        for (int i = 0; i < 8; ++i)
+            if (i < per4) {
+                const int e = 4 * (tid + i * nthr);
+                if (e < T * T) {
+                    const int rr = e / T, cc = e - rr * T;
+                    *reinterpret_cast<float4 *>(As + rr * P + cc) = ra[i];
+                    *reinterpret_cast<float4 *>(Bs + rr * P + cc) = rb[i];
+                }
             }
-        }
+        __syncthreads();
+        if (k0 + T < n) fetch(k0 + T);
         for (int kk = 0; kk < T; kk += 4) {
-            const float b0 = Bs[(kk + 0) * T + tx], b1 = Bs[(kk + 1) * T + tx];
-            const float b2 = Bs[(kk + 2) * T + tx], b3 = Bs[(kk + 3) * T + tx];
+            V b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) b[u] = *reinterpret_cast<const V *>(Bs + (kk + u) * P + CC * tx);
 #pragma unroll
             for (int r = 0; r < W; ++r) {
-                const float4 a = *reinterpret_cast<const float4 *>(As + (ty + r * h) * PA + kk);
-                acc[r] = __fmaf_rn(a.x, b0, acc[r]);
-                acc[r] = __fmaf_rn(a.y, b1, acc[r]);
-                acc[r] = __fmaf_rn(a.z, b2, acc[r]);
-                acc[r] = __fmaf_rn(a.w, b3, acc[r]);
+                const float4 a = *reinterpret_cast<const float4 *>(As + (ty + r * h) * P + kk);
+                const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int q = 0; q < CC; ++q) acc[r][q] = __fmaf_rn(av[u], vget<CC>(b[u], q), acc[r][q]);
             }
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < W; ++r) C[(size_t)(blockIdx.y * T + ty + r * h) * n + col] = acc[r];
+    for (int r = 0; r < W; ++r)
+#pragma unroll
+        for (int q = 0; q < CC; ++q) C[(size_t)(row0 + ty + r * h) * n + col0 + CC * tx + q] = acc[r][q];
 }
 
 // ------------------------------------------------------------ convolution-separable
