@@ -607,7 +607,7 @@ def run_rf(args, L, world, rank, barrier, gather_max_sum):
     held = ev["held_idx"]
     mine = np.array_split(held, world)[rank]
     rec = table.records(mine)
-    L.features_records(rec[:64])  # warm-up
+    L.features_records(rec)  # warm-up (first call: module load and the stream-ordered pool's growth)
     barrier()
     t0 = time.perf_counter()
     fb = L.features_records(rec)

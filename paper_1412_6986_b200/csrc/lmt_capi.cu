@@ -1731,7 +1731,6 @@ std::string real_violations(const lmt_real_instance &r) {
                 return "matrixMul needs tile <= 64, a multiple of 4 dividing n, wg_x | tile, wg_y | tile";
             if (T / wy != 1 && T / wy != 2 && T / wy != 4 && T / wy != 8) return "matrixMul rows per thread tile/wg_y must be 1, 2, 4 or 8";
             if (T / wx != 1 && T / wx != 2 && T / wx != 4) return "matrixMul columns per thread tile/wg_x must be 1, 2 or 4";
-            if ((T * T / 4 + wx * wy - 1) / (wx * wy) > 8) return "matrixMul tile copy needs at most 8 float4 per thread";
             return "";
         case 2:
             if (T < 1) return "convolution outputs per thread (tile) must be >= 1";

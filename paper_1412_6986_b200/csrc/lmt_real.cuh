@@ -95,7 +95,8 @@ __global__ void k_transpose_opt(const float *__restrict__ A, float *__restrict__
 // CC-wide read of B[k][cols] per k feed 4 * W * CC FMAs, so a thread's
 // register tile costs W + 4 loads per 4 k instead of 2 per FMA.
 template <int CC>
-__global__ void k_matmul_base(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
+__global__ void __launch_bounds__(1024) k_matmul_base(const float *__restrict__ A, const float *__restrict__ B,
+                                                      float *__restrict__ C,
                               int n, int T, int W) {
     using V = typename VecOf<CC>::T;
     const int h = T / W;
@@ -130,9 +131,10 @@ __global__ void k_matmul_base(const float *__restrict__ A, const float *__restri
 // optimized: A and B tiles staged in shared memory (rows padded to T + 4
 // floats: 16-byte aligned for the 128-bit reads), the next tiles' elements
 // loaded into registers while the current tiles are consumed.
+// launch bounds: the most threads a tile of <= 64 x 64 needs at this W x CC
 template <int W, int CC>
-__global__ void k_matmul_opt(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C,
-                             int n, int T) {
+__global__ void __launch_bounds__(4096 / (W * CC) < 1024 ? 4096 / (W * CC) : 1024)
+    k_matmul_opt(const float *__restrict__ A, const float *__restrict__ B, float *__restrict__ C, int n, int T) {
     using V = typename VecOf<CC>::T;
     extern __shared__ __align__(16) float sm[];  // As[T][T + 4], Bs[T][T + 4]
     const int P = T + 4, h = T / W;
@@ -140,18 +142,19 @@ __global__ void k_matmul_opt(const float *__restrict__ A, const float *__restric
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int nthr = blockDim.x * blockDim.y, tid = ty * blockDim.x + tx;
     const int col0 = blockIdx.x * T, row0 = blockIdx.y * T;
-    // tile copy: each thread moves (T * T) / nthr elements of A and of B per
-    // k-tile, four at a time (T % 4 == 0): element e = 4 * (tid + i * nthr)
+    // tile copy: each thread moves (T * T) / nthr = W * CC elements of A and
+    // of B per k-tile, four at a time (T % 4 == 0): element e = 4 * (tid + i * nthr)
+    constexpr int NF = (W * CC + 3) / 4;  // float4 per thread per tile
     const int per4 = (T * T / 4 + nthr - 1) / nthr;
     float acc[W][CC];
 #pragma unroll
     for (int r = 0; r < W; ++r)
 #pragma unroll
         for (int q = 0; q < CC; ++q) acc[r][q] = 0.0f;
-    float4 ra[8], rb[8];  // up to 8 float4 per thread per tile (T <= 64, >= 128 threads; T <= 32: >= 32)
+    float4 ra[NF], rb[NF];
     auto fetch = [&](int k0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < NF; ++i)
             if (i < per4) {
                 const int e = 4 * (tid + i * nthr);
                 if (e < T * T) {
@@ -164,7 +167,7 @@ __global__ void k_matmul_opt(const float *__restrict__ A, const float *__restric
     fetch(0);
     for (int k0 = 0; k0 < n; k0 += T) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < NF; ++i)
             if (i < per4) {
                 const int e = 4 * (tid + i * nthr);
                 if (e < T * T) {
