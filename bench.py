@@ -608,6 +608,9 @@ def run_rf(args, L, world, rank, barrier, gather_max_sum):
     mine = np.array_split(held, world)[rank]
     rec = table.records(mine)
     L.features_records(rec)  # warm-up (first call: module load and the stream-ordered pool's growth)
+    import gc
+
+    gc.collect()
     barrier()
     t0 = time.perf_counter()
     fb = L.features_records(rec)
@@ -731,6 +734,12 @@ def run_e2e(args, L, table, steps_rows, mode, world, rank, barrier, gather_max_s
         t0 += time.perf_counter() - t_check  # the check is not part of the timed path
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
+    # release the pinned staging buffers now: freeing GBs of pinned memory is
+    # slow and would otherwise land inside a later leg's timed region
+    del host_in, ring, in2_host
+    import gc
+
+    gc.collect()
     (el,), (n_all, checked, bad) = gather_max_sum([el], [n, checked, bad])
     return {"value": n_all / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d / len(plan)),
             "d2h_bytes_per_step": int(d2h / len(plan)), "steps": len(plan), "instances": int(n_all),
