@@ -815,7 +815,11 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
     const bool membound = pl->alg_bytes / 6.5e12 >= issue_s && ctas >= 2 * sms;
     int64_t maxt_b = maxt, minb = 1;
     if ((nit <= 2 || membound) && ctas >= 2 * sms) {
-        minb = std::min<int64_t>({(32 + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
+        // memory-bound: 32 resident warps per SM; a compute chain with few
+        // units per thread: 16 (forcing 32 spilled the U = 2 body to U = 1 on a
+        // launch of 4-thread workgroups: 85 -> 69 ms at 16, profiles/r02_tune_tiny.json)
+        const int64_t want = membound ? 32 : 16;
+        minb = std::min<int64_t>({(want + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
                                   ctas / std::max<int64_t>(1, sms)});
         if (minb > 1) maxt_b = warps * 32;
         else minb = 1;
