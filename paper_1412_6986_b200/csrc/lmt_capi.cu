@@ -360,6 +360,14 @@ int get_ctx(DevCtx **out) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma<32>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        for (const void *kf : {reinterpret_cast<const void *>(k_matmul_opt_t<64, 4, 4>),
+                               reinterpret_cast<const void *>(k_matmul_opt_t<64, 8, 4>)})
+            CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        for (const void *kf : {reinterpret_cast<const void *>(k_mvt1_ring<16>), reinterpret_cast<const void *>(k_mvt1_ring<32>),
+                               reinterpret_cast<const void *>(k_mvt2_ring<16, 32>), reinterpret_cast<const void *>(k_mvt2_ring<16, 64>),
+                               reinterpret_cast<const void *>(k_mvt2_ring<16, 128>), reinterpret_cast<const void *>(k_mvt2_ring<32, 32>),
+                               reinterpret_cast<const void *>(k_mvt2_ring<32, 64>), reinterpret_cast<const void *>(k_mvt2_ring<32, 128>)})
+            CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         for (const void *kf : {reinterpret_cast<const void *>(k_conv_rows_opt<0>), reinterpret_cast<const void *>(k_conv_rows_opt<1>),
                                reinterpret_cast<const void *>(k_conv_rows_opt<2>), reinterpret_cast<const void *>(k_conv_rows_opt<4>),
                                reinterpret_cast<const void *>(k_conv_rows_opt<8>), reinterpret_cast<const void *>(k_conv_cols_opt<0>),
@@ -1762,6 +1770,129 @@ RealConv real_weights(int R) {
     return c;
 }
 
+// MVT: the side stream kernel 2 runs on (per device, created on first use;
+// callers hold g_mu)
+struct RealSide {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int sms = 0;
+};
+RealSide g_real_side[64];
+
+RealSide &real_side() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    RealSide &sd = g_real_side[dev];
+    if (!sd.s) {
+        cudaStream_t st = nullptr;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sd.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return sd;
+        sd.s = st;
+    }
+    return sd;
+}
+
+// tensor map of the n x n matrix A (fp32, row-major) with a box of bx columns x by rows
+int mvt_tmap(RealTmap *t, const float *A, int n, int bx, int by) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)n * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult e = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(A), dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (e != CUDA_SUCCESS) return fail(LMT_ERR_CUDA, "MVT tensor map (%d)", (int)e);
+    *t = *reinterpret_cast<const RealTmap *>(&m);
+    return LMT_OK;
+}
+
+// MVT optimized variant: kernel 1 on s, kernel 2 on the side stream. When
+// the two grids together exceed the SM count (32-row workgroups: 2 x 128
+// CTAs), each kernel's ring is sized to half an SM's shared memory so one CTA
+// of each can share an SM; otherwise each CTA has an SM to itself.
+int mvt_opt_launch(const lmt_real_instance &r, const float *const *in, float *out, cudaStream_t s, const RealSide &sd,
+                   int smem_optin) {
+    const int n = r.n, wx = r.wg_x, T = r.tile;
+    const dim3 grd(n / wx);
+    const int64_t ybytes = (int64_t)n * 4;
+    const bool share = 2 * (n / wx) > sd.sms;
+    const int64_t budget = share ? 110 * 1024 : smem_optin - 2048;
+    // kernel 1: ring kernel for workgroups of <= 128 rows (stages of 128 + 4 columns)
+    const int64_t st1 = (int64_t)wx * (kMvtRingCols + 4) * 4;
+    const int S1 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, (budget - 128 - ybytes) / st1, (int64_t)n / kMvtRingCols});
+    const int64_t st2 = (int64_t)wx * kMvtRingRows * 4;
+    const int S2 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, (budget - 128 - ybytes) / st2, (int64_t)n / kMvtRingRows});
+    const bool ring1 = wx <= 128 && n % kMvtRingCols == 0 && S1 >= 2;
+    const bool ring2 = (wx == 32 || wx == 64 || wx == 128) && n % kMvtRingRows == 0 && S2 >= 2;
+    if (ring1) {
+        RealTmap t1;
+        if (int rc = mvt_tmap(&t1, in[0], n, kMvtRingCols + 4, wx)) return rc;
+        const size_t sm = (size_t)S1 * st1 + 128 + ybytes;
+        if (T == 32) k_mvt1_ring<32><<<grd, wx, sm, s>>>(t1, in[1], in[3], out, n, S1);
+        else k_mvt1_ring<16><<<grd, wx, sm, s>>>(t1, in[1], in[3], out, n, S1);
+    }
+    if (ring2) {
+        RealTmap t2;
+        if (int rc = mvt_tmap(&t2, in[0], n, wx, kMvtRingRows)) return rc;
+        const size_t sm = (size_t)S2 * st2 + 128 + ybytes;
+#define LMT_MVT2(TT, W_) \
+    if (T == TT && wx == W_) k_mvt2_ring<TT, W_><<<grd, wx, sm, sd.s>>>(t2, in[2], in[4], out + n, n, S2);
+        LMT_MVT2(16, 32) LMT_MVT2(16, 64) LMT_MVT2(16, 128) LMT_MVT2(32, 32) LMT_MVT2(32, 64) LMT_MVT2(32, 128)
+#undef LMT_MVT2
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (ring1 && ring2) return LMT_OK;
+    // wide workgroups (few CTAs: each has an SM to itself): the general ring kernels
+    // A streamed through a ring of S stages of [wg][T] (kernel 1) and [T][wg] (kernel 2)
+    // tiles by TMA; y is staged whole in shared memory after each kernel's ring
+    const int64_t stage = (int64_t)wx * T * 4, cap = smem_optin - 2048 - (int64_t)n * 4;
+    const int S = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage, (int64_t)n / T});
+    // kernel 1: stages of NB boxes of bwu + 4 columns (2 x 128 when two stages fit,
+    // else one box, then narrower ones for wide workgroups)
+    int bwu = kMvtBoxCols, NB = kMvtStageCols / kMvtBoxCols;
+    auto st1f = [&]() { return (int64_t)wx * (bwu + 4) * 4 * NB; };
+    while (st1f() * 2 > cap && (NB > 1 || bwu > 16)) {
+        if (NB > 1) NB--;
+        else bwu >>= 1;
+    }
+    const int64_t stage1 = st1f();
+    const int S1w = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage1, (int64_t)n / (NB * bwu)});
+    if (S < 1 || S1w < 1 || n % (NB * bwu))
+        return fail(LMT_ERR_TOO_LARGE, "MVT needs n %% %d == 0 and %lld bytes of shared memory per stage", NB * bwu,
+                    (long long)stage1);
+    if (!ring1) {
+        RealTmap t1;
+        if (int rc = mvt_tmap(&t1, in[0], n, bwu + 4, std::min(wx, 256))) return rc;
+        int bwl = 0;
+        while ((1 << bwl) < bwu) bwl++;
+        const size_t sm = (size_t)S1w * stage1 + 128 + ybytes;
+        if (T == 32 && wx <= 256 && bwu >= 32)
+            k_mvt1_tma<32><<<grd, wx, sm, s>>>(t1, in[1], in[3], out, n, S1w, bwl, NB);
+        else
+            k_mvt1_tma<16><<<grd, wx, sm, s>>>(t1, in[1], in[3], out, n, S1w, bwl, NB);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (!ring2) {
+        if (T == 32 && wx <= 256) {
+            RealTmap t2;
+            if (int rc = mvt_tmap(&t2, in[0], n, std::min(wx, 256), T)) return rc;
+            k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128 + ybytes, sd.s>>>(t2, in[2], in[4], out + n, n, S);
+        } else {  // T = 16 stages (same results: T only sets the staging granularity)
+            const int64_t stage16 = (int64_t)wx * 16 * 4;
+            const int S16 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage16, (int64_t)n / 16});
+            RealTmap t2;
+            if (int rc = mvt_tmap(&t2, in[0], n, std::min(wx, 256), 16)) return rc;
+            k_mvt2_tma<16><<<grd, wx, (size_t)S16 * stage16 + 128 + ybytes, sd.s>>>(t2, in[2], in[4], out + n, n, S16);
+        }
+        CUDA_TRY(cudaGetLastError());
+    }
+    return LMT_OK;
+}
+
 // inputs: transpose {A}; matrixMul {A, B}; convolution {in} (+ scratch `tmp`
 // of n*n floats); MVT {A, y1, y2, x1_0, x2_0}; out: n*n floats, MVT 2n (x1 then x2)
 int real_launch(const lmt_real_instance &r, int variant, const float *const *in, float *out, float *tmp,
@@ -1793,6 +1924,17 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
                 else k_matmul_base<4><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
                 break;
             }
+            // compile-time tile shapes (the instance set's T = 16, 32, 64): double-buffered
+#define LMT_MMT(TT, WW, C_)                                                                                 \
+    if (T == TT && W == WW && CC == C_) {                                                                   \
+        k_matmul_opt_t<TT, WW, C_><<<grd, blk, (size_t)4 * TT * (TT + 4) * 4, s>>>(in[0], in[1], out, n); \
+        break;                                                                                              \
+    }
+            LMT_MMT(16, 1, 1) LMT_MMT(16, 2, 1) LMT_MMT(16, 4, 1) LMT_MMT(16, 8, 1)
+            LMT_MMT(32, 1, 1) LMT_MMT(32, 2, 1) LMT_MMT(32, 4, 1) LMT_MMT(32, 8, 1)
+            LMT_MMT(32, 8, 2) LMT_MMT(32, 4, 4) LMT_MMT(32, 8, 4)
+            LMT_MMT(64, 4, 4) LMT_MMT(64, 8, 4)
+#undef LMT_MMT
             const size_t sm = (size_t)2 * T * (T + 4) * 4;
 #define LMT_MM(WW, C_)                                                                    \
     if (W == WW && CC == C_) {                                                            \
@@ -1829,73 +1971,25 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
             break;
         }
         case 3: {
+            // kernel 1 (x1, row dots) and kernel 2 (x2, column dots) are independent
+            // (Polybench launches them back to back): both variants run them
+            // concurrently, kernel 2 on a side stream forked from and joined back
+            // into `s`, so the events around a variant bracket both
+            RealSide &sd = real_side();
+            if (!sd.s) return fail(LMT_ERR_CUDA, "MVT side stream");
+            CUDA_TRY(cudaEventRecord(sd.fork, s));
+            CUDA_TRY(cudaStreamWaitEvent(sd.s, sd.fork, 0));
             const dim3 grd(n / wx);
             if (variant == 0) {
                 k_mvt1_base<<<grd, wx, 0, s>>>(in[0], in[1], in[3], out, n);
-                k_mvt2_base<<<grd, wx, 0, s>>>(in[0], in[2], in[4], out + n, n);
+                k_mvt2_base<<<grd, wx, 0, sd.s>>>(in[0], in[2], in[4], out + n, n);
             } else {
-                // A streamed through a ring of S stages of [wg][T] (kernel 1, swizzled
-                // 64/128-byte rows) and [T][wg] (kernel 2) tiles by TMA
-                // y is staged whole in shared memory after each kernel's ring
-                const int64_t stage = (int64_t)wx * T * 4, cap = smem_optin - 2048 - (int64_t)n * 4;
-                const int S = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage, (int64_t)n / T});
-                // kernel 1: stages of NB boxes of bwu + 4 columns (2 x 128 when two stages fit,
-                // else one box, then narrower ones for wide workgroups)
-                int bwu = kMvtBoxCols, NB = kMvtStageCols / kMvtBoxCols;
-                auto st1 = [&]() { return (int64_t)wx * (bwu + 4) * 4 * NB; };
-                while (st1() * 2 > cap && (NB > 1 || bwu > 16)) {
-                    if (NB > 1) NB--;
-                    else bwu >>= 1;
-                }
-                const int64_t stage1 = st1();
-                const int S1 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage1, (int64_t)n / (NB * bwu)});
-                if (S < 1 || S1 < 1 || n % (NB * bwu))
-                    return fail(LMT_ERR_TOO_LARGE, "MVT needs n %% %d == 0 and %lld bytes of shared memory per stage",
-                                NB * bwu, (long long)stage1);
-                CUtensorMap m1, m2;
-                const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
-                const cuuint64_t strides[1] = {(cuuint64_t)n * 4};
-                const cuuint32_t estr[2] = {1, 1};
-                const cuuint32_t box1[2] = {(cuuint32_t)(bwu + 4), (cuuint32_t)std::min(wx, 256)};
-                const cuuint32_t box2[2] = {(cuuint32_t)std::min(wx, 256), (cuuint32_t)T};
-                const CUresult e1 = g_encode(&m1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(in[0]), dims,
-                                             strides, box1, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-                const CUresult e2 = g_encode(&m2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(in[0]), dims,
-                                             strides, box2, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-                if (e1 != CUDA_SUCCESS || e2 != CUDA_SUCCESS)
-                    return fail(LMT_ERR_CUDA, "MVT tensor maps: %d %d", (int)e1, (int)e2);
-                const RealTmap t1 = *reinterpret_cast<const RealTmap *>(&m1);
-                const RealTmap t2 = *reinterpret_cast<const RealTmap *>(&m2);
-                // kernel 2 with 16-row stages (T = 16, or wide workgroups of T = 32)
-                const int64_t stage16 = (int64_t)wx * 16 * 4;
-                const int S16 = (int)std::min<int64_t>({(int64_t)kMvtMaxStages, cap / stage16, (int64_t)n / 16});
-                RealTmap t2x = t2;
-                if (T == 32 && wx > 256) {
-                    CUtensorMap m3;
-                    const cuuint32_t box3[2] = {(cuuint32_t)std::min(wx, 256), 16u};
-                    if (g_encode(&m3, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(in[0]), dims, strides, box3,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-                        return fail(LMT_ERR_CUDA, "MVT tensor map");
-                    t2x = *reinterpret_cast<const RealTmap *>(&m3);
-                }
-                const size_t ybytes = (size_t)n * 4;
-                int bwl = 0;
-                while ((1 << bwl) < bwu) bwl++;
-                if (T == 32 && wx <= 256 && bwu >= 32)
-                    k_mvt1_tma<32><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwl, NB);
-                else
-                    k_mvt1_tma<16><<<grd, wx, (size_t)S1 * stage1 + 128 + ybytes, s>>>(t1, in[1], in[3], out, n, S1, bwl, NB);
-                CUDA_TRY(cudaGetLastError());
-                if (T == 32 && wx <= 256)
-                    k_mvt2_tma<32><<<grd, wx, (size_t)S * stage + 128 + ybytes, s>>>(t2, in[2], in[4], out + n, n, S);
-                else  // T = 16 stages (same results: T only sets the staging granularity)
-                    k_mvt2_tma<16><<<grd, wx, (size_t)S16 * stage16 + 128 + ybytes, s>>>(t2x, in[2], in[4], out + n, n, S16);
+                const int rc = mvt_opt_launch(r, in, out, s, sd, smem_optin);
+                if (rc) return rc;
             }
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaEventRecord(sd.join, sd.s));
+            CUDA_TRY(cudaStreamWaitEvent(s, sd.join, 0));
             break;
         }
     }

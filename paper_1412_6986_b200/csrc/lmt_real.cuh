@@ -200,6 +200,94 @@ __global__ void __launch_bounds__(4096 / (W * CC) < 1024 ? 4096 / (W * CC) : 102
         for (int q = 0; q < CC; ++q) C[(size_t)(row0 + ty + r * h) * n + col0 + CC * tx + q] = acc[r][q];
 }
 
+// optimized, tile shape compile-time (T, W, CC of the instance set): the tile
+// copy's index math folds to shifts, the k loop over a tile unrolls fully,
+// and two shared-memory buffers take one barrier per k-tile (the next
+// tiles go from registers into the other buffer while this one is read).
+// Same per-output order as k_matmul_opt (k ascending, one fmaf each).
+template <int T, int W, int CC>
+__global__ void __launch_bounds__((T / CC) * (T / W)) k_matmul_opt_t(const float *__restrict__ A,
+                                                                    const float *__restrict__ B,
+                                                                    float *__restrict__ C, int n) {
+    using V = typename VecOf<CC>::T;
+    constexpr int TX = T / CC, TY = T / W, NT = TX * TY, P = T + 4;
+    constexpr int E4 = T * T / 4;             // float4 per tile
+    constexpr int NF = (E4 + NT - 1) / NT;    // float4 per thread per tile
+    extern __shared__ __align__(16) float sm[];  // [2][As[T][P], Bs[T][P]]
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int col0 = blockIdx.x * T, row0 = blockIdx.y * T;
+    float acc[W][CC];
+#pragma unroll
+    for (int r = 0; r < W; ++r)
+#pragma unroll
+        for (int q = 0; q < CC; ++q) acc[r][q] = 0.0f;
+    float4 ra[NF], rb[NF];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int e = tid + i * NT;
+            if (E4 % NT == 0 || e < E4) {
+                const int rr = e / (T / 4), cc = (e % (T / 4)) * 4;
+                ra[i] = __ldg(reinterpret_cast<const float4 *>(A + (size_t)(row0 + rr) * n + k0 + cc));
+                rb[i] = __ldg(reinterpret_cast<const float4 *>(B + (size_t)(k0 + rr) * n + col0 + cc));
+            }
+        }
+    };
+    auto store = [&](int b) {
+        float *As = sm + b * 2 * T * P, *Bs = As + T * P;
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int e = tid + i * NT;
+            if (E4 % NT == 0 || e < E4) {
+                const int rr = e / (T / 4), cc = (e % (T / 4)) * 4;
+                *reinterpret_cast<float4 *>(As + rr * P + cc) = ra[i];
+                *reinterpret_cast<float4 *>(Bs + rr * P + cc) = rb[i];
+            }
+        }
+    };
+    const int nt = n / T;
+    fetch(0);
+    store(0);
+    __syncthreads();
+    for (int t = 0; t < nt; ++t) {
+        if (t + 1 < nt) fetch((t + 1) * T);
+        const float *As = sm + (t & 1) * 2 * T * P, *Bs = As + T * P;
+        // the fragments of k-step kk + 4 are read from shared memory while
+        // the FMAs of kk run (ncu: short_scoreboard was half the stalls)
+        V bq[2][4];
+        float4 aq[2][W];
+        auto frag = [&](int b, int kk) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bq[b][u] = *reinterpret_cast<const V *>(Bs + (kk + u) * P + CC * tx);
+#pragma unroll
+            for (int r = 0; r < W; ++r) aq[b][r] = *reinterpret_cast<const float4 *>(As + (ty + r * TY) * P + kk);
+        };
+        frag(0, 0);
+#pragma unroll
+        for (int kk = 0; kk < T; kk += 4) {
+            const int cb = (kk >> 2) & 1;
+            if (kk + 4 < T) frag(cb ^ 1, kk + 4);
+#pragma unroll
+            for (int r = 0; r < W; ++r) {
+                const float av[4] = {aq[cb][r].x, aq[cb][r].y, aq[cb][r].z, aq[cb][r].w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int q = 0; q < CC; ++q) acc[r][q] = __fmaf_rn(av[u], vget<CC>(bq[cb][u], q), acc[r][q]);
+            }
+        }
+        if (t + 1 < nt) store((t + 1) & 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < W; ++r) {
+        V v;
+#pragma unroll
+        for (int q = 0; q < CC; ++q) vset<CC>(v, q, acc[r][q]);
+        *reinterpret_cast<V *>(C + (size_t)(row0 + ty + r * TY) * n + col0 + CC * tx) = v;
+    }
+}
+
 // ------------------------------------------------------------ convolution-separable
 // rows: out[y][x] = sum_{k=-R..R} in[y][x+k] * w[R-k]; cols: out[y][x] = sum_k in[y+k][x] * w[R-k];
 // taps outside the image read 0. blockDim (wx, wy); each thread computes W
@@ -214,6 +302,17 @@ __global__ void k_conv_rows_base(const float *__restrict__ in, float *__restrict
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int x0 = blockIdx.x * blockDim.x * W + threadIdx.x;
     const float *row = in + (size_t)y * n;
+    const int xb = blockIdx.x * blockDim.x * W;
+    if (xb >= R && xb + (int)blockDim.x * W + R <= n) {  // CTA-uniform: every tap inside the image
+        for (int q = 0; q < W; ++q) {
+            const int x = x0 + q * blockDim.x;
+            float acc = 0.0f;
+#pragma unroll
+            for (int k = -R; k <= R; ++k) acc = __fmaf_rn(__ldg(row + x + k), c.w[R - k], acc);
+            out[(size_t)y * n + x] = acc;
+        }
+        return;
+    }
     for (int q = 0; q < W; ++q) {
         const int x = x0 + q * blockDim.x;
         float acc = 0.0f;
@@ -233,6 +332,18 @@ __global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict
     const int R = RR ? RR : Rr;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y0 = blockIdx.y * blockDim.y * W + threadIdx.y;
+    const int yb = blockIdx.y * blockDim.y * W;
+    if (yb >= R && yb + (int)blockDim.y * W + R <= n) {  // CTA-uniform: every tap inside the image
+        for (int q = 0; q < W; ++q) {
+            const int y = y0 + q * blockDim.y;
+            const float *col = in + (size_t)y * n + x;
+            float acc = 0.0f;
+#pragma unroll
+            for (int k = -R; k <= R; ++k) acc = __fmaf_rn(__ldg(col + (ptrdiff_t)k * n), c.w[R - k], acc);
+            out[(size_t)y * n + x] = acc;
+        }
+        return;
+    }
     for (int q = 0; q < W; ++q) {
         const int y = y0 + q * blockDim.y;
         float acc = 0.0f;
@@ -643,6 +754,179 @@ __global__ void __launch_bounds__(T == 32 ? 256 : 512) k_mvt2_tma(const __grid_c
 #undef MVT2_LOAD
 #undef MVT2_FMA
 #undef MVT2_STEP
+    x2[i0 + tid] = acc;
+}
+
+// ---- MVT ring kernels with compile-time stages (workgroups of <= 128 rows /
+// columns; the kernels above stay for the wider ones). ncu on the kernels
+// above: the only warp of an SM spent ~18 cycles per element, 15.6k
+// instructions for 4,096 FMAs -- per-sub-step bookkeeping (which slot,
+// which phase, is this the last sub-step) issued between the chain's FFMAs.
+// Here a stage is a compile-time number of T-wide sub-steps, unrolled: the
+// next sub-step's shared-memory loads are issued between the current FFMAs
+// and the ring bookkeeping runs once per stage.
+constexpr int kMvtRingCols = 128;  // kernel 1: columns per stage (one TMA box of 128 + 4 columns)
+constexpr int kMvtRingRows = 128;  // kernel 2: rows per stage (one TMA box of 128 rows x wg columns)
+
+template <int T>
+__global__ void __launch_bounds__(128) k_mvt1_ring(const __grid_constant__ RealTmap tm, const float *__restrict__ y1,
+                                                  const float *__restrict__ x1_0, float *__restrict__ x1, int n,
+                                                  int S) {
+    constexpr int BW = kMvtRingCols + 4;  // staged row pitch: 528 bytes = 33 x 16 (conflict-free 128-bit reads)
+    constexpr int KB = kMvtRingCols / T;  // sub-steps per stage
+    static_assert(KB % 2 == 0, "stages start on register buffer 0");
+    extern __shared__ unsigned char rk_raw[];
+    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
+    float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
+    const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int i0 = blockIdx.x * wg, steps = n / kMvtRingCols;
+    const int sf = wg * BW;  // floats per stage
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            rk_bar_init(&full[s], 1);
+            rk_bar_init(&empty[s], wg / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int slot, int step) {
+        rk_expect(&full[slot], (unsigned)(sf * 4));
+        rk_tma2d(st + slot * sf, &tm, &full[slot], step * kMvtRingCols, i0);
+    };
+    if (tid == 0)
+        for (int s = 0; s < S && s < steps; ++s) issue(s, s);
+    float *ys = st + (size_t)S * sf;
+    rk_stage_vec(ys, y1, n, tid, wg);
+    __syncthreads();
+    const unsigned yb = rk_smem(ys);
+    const unsigned rowb = rk_smem(st) + (unsigned)(tid * BW * 4);
+    float acc = x1_0[i0 + tid];
+    float4 a[2][T / 4], y[2][T / 4];
+    auto load = [&](int b, unsigned pa, unsigned py) {
+#pragma unroll
+        for (int c = 0; c < T / 4; ++c) {
+            a[b][c] = rk_lds4(pa + (unsigned)(c << 4));
+            y[b][c] = rk_lds4(py + (unsigned)(c << 4));
+        }
+    };
+    int slot = 0;
+    unsigned phase = 0;
+    rk_wait(&full[0], 0);
+    load(0, rowb, yb);
+    for (int step = 0; step < steps; ++step) {
+        const unsigned sb = rowb + (unsigned)(slot * sf * 4);
+        const unsigned ysb = yb + (unsigned)(step * kMvtRingCols * 4);
+        int ns = slot + 1;
+        unsigned nph = phase;
+        if (ns == S) {
+            ns = 0;
+            nph ^= 1;
+        }
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            if (kb + 1 < KB) {
+                load((kb + 1) & 1, sb + (unsigned)((kb + 1) * T * 4), ysb + (unsigned)((kb + 1) * T * 4));
+            } else if (step + 1 < steps) {  // the next stage's first sub-step
+                rk_wait(&full[ns], nph);
+                load(0, rowb + (unsigned)(ns * sf * 4), ysb + (unsigned)(kMvtRingCols * 4));
+            }
+#pragma unroll
+            for (int c = 0; c < T / 4; ++c) {
+                acc = __fmaf_rn(a[kb & 1][c].x, y[kb & 1][c].x, acc);
+                acc = __fmaf_rn(a[kb & 1][c].y, y[kb & 1][c].y, acc);
+                acc = __fmaf_rn(a[kb & 1][c].z, y[kb & 1][c].z, acc);
+                acc = __fmaf_rn(a[kb & 1][c].w, y[kb & 1][c].w, acc);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) rk_arrive(&empty[slot]);
+        if (tid == 0 && step + S < steps) {
+            rk_wait(&empty[slot], phase);
+            issue(slot, step + S);
+        }
+        slot = ns;
+        phase = nph;
+    }
+    x1[i0 + tid] = acc;
+}
+
+template <int T, int WG>
+__global__ void __launch_bounds__(WG) k_mvt2_ring(const __grid_constant__ RealTmap tm, const float *__restrict__ y2,
+                                                 const float *__restrict__ x2_0, float *__restrict__ x2, int n, int S) {
+    constexpr int KB = kMvtRingRows / T;
+    constexpr int sf = WG * kMvtRingRows;  // floats per stage: [128 rows][WG columns]
+    static_assert(KB % 2 == 0, "stages start on register buffer 0");
+    extern __shared__ unsigned char rk_raw[];
+    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
+    float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int i0 = blockIdx.x * WG, steps = n / kMvtRingRows;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            rk_bar_init(&full[s], 1);
+            rk_bar_init(&empty[s], WG / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int slot, int step) {
+        rk_expect(&full[slot], (unsigned)(sf * 4));
+        rk_tma2d(st + slot * sf, &tm, &full[slot], i0, step * kMvtRingRows);
+    };
+    if (tid == 0)
+        for (int s = 0; s < S && s < steps; ++s) issue(s, s);
+    float *ys = st + (size_t)S * sf;
+    rk_stage_vec(ys, y2, n, tid, WG);
+    __syncthreads();
+    const unsigned yb = rk_smem(ys);
+    const unsigned colb = rk_smem(st) + (unsigned)(tid * 4);
+    float acc = x2_0[i0 + tid];
+    float a[2][T];
+    float4 y[2][T / 4];
+    auto load = [&](int b, unsigned pa, unsigned py) {
+#pragma unroll
+        for (int jj = 0; jj < T; ++jj) a[b][jj] = rk_lds(pa + (unsigned)(jj * WG * 4));
+#pragma unroll
+        for (int q = 0; q < T / 4; ++q) y[b][q] = rk_lds4(py + (unsigned)(q << 4));
+    };
+    int slot = 0;
+    unsigned phase = 0;
+    rk_wait(&full[0], 0);
+    load(0, colb, yb);
+    for (int step = 0; step < steps; ++step) {
+        const unsigned sb = colb + (unsigned)(slot * sf * 4);
+        const unsigned ysb = yb + (unsigned)(step * kMvtRingRows * 4);
+        int ns = slot + 1;
+        unsigned nph = phase;
+        if (ns == S) {
+            ns = 0;
+            nph ^= 1;
+        }
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            if (kb + 1 < KB) {
+                load((kb + 1) & 1, sb + (unsigned)((kb + 1) * T * WG * 4), ysb + (unsigned)((kb + 1) * T * 4));
+            } else if (step + 1 < steps) {
+                rk_wait(&full[ns], nph);
+                load(0, colb + (unsigned)(ns * sf * 4), ysb + (unsigned)(kMvtRingRows * 4));
+            }
+#pragma unroll
+            for (int q = 0; q < T / 4; ++q) {
+                acc = __fmaf_rn(a[kb & 1][4 * q + 0], y[kb & 1][q].x, acc);
+                acc = __fmaf_rn(a[kb & 1][4 * q + 1], y[kb & 1][q].y, acc);
+                acc = __fmaf_rn(a[kb & 1][4 * q + 2], y[kb & 1][q].z, acc);
+                acc = __fmaf_rn(a[kb & 1][4 * q + 3], y[kb & 1][q].w, acc);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) rk_arrive(&empty[slot]);
+        if (tid == 0 && step + S < steps) {
+            rk_wait(&empty[slot], phase);
+            issue(slot, step + S);
+        }
+        slot = ns;
+        phase = nph;
+    }
     x2[i0 + tid] = acc;
 }
 

@@ -26,6 +26,7 @@ __global__ void probe(float *out, long long *cycles, int iters, float c2r) {
                 }
                 if (FORM == 3) acc[u] = __fmaf_rn(acc[u], (k & 1) ? 0.5f : 2.0f, (k & 1) ? -0.03125f : 0.015625f);
                 if (FORM == 4) acc[u] = __fmaf_rn(acc[u], (k & 1) ? 0.5f : 2.0f, c2r);  // imm c1, reg c2
+                if (FORM == 5) acc[u] = __fmaf_rn(x, c2r, acc[u]);                     // FFMA R,R,R (matmul form)
             }
         }
     }
@@ -65,6 +66,8 @@ int main() {
         run<8, 3>("FFMA const c1,c2", w);
         run<8, 4>("FFMA imm c1, reg c2", w);
         run<16, 0>("FADD R,R,R", w);
+        run<8, 5>("FFMA R,R,R", w);
+        run<16, 5>("FFMA R,R,R", w);
     }
     return 0;
 }
