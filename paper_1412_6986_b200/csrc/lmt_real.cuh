@@ -765,6 +765,13 @@ __global__ void __launch_bounds__(T == 32 ? 256 : 512) k_mvt2_tma(const __grid_c
 // Here a stage is a compile-time number of T-wide sub-steps, unrolled: the
 // next sub-step's shared-memory loads are issued between the current FFMAs
 // and the ring bookkeeping runs once per stage.
+// one 1D bulk copy global -> shared (bytes % 16 == 0, both 16-byte aligned)
+__device__ __forceinline__ void rk_bulk(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     rk_smem(dst)),
+                 "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(rk_smem(bar))
+                 : "memory");
+}
 constexpr int kMvtRingCols = 128;  // kernel 1: columns per stage (one TMA box of 128 + 4 columns)
 constexpr int kMvtRingRows = 128;  // kernel 2: rows per stage (one TMA box of 128 rows x wg columns)
 
@@ -776,16 +783,18 @@ __global__ void __launch_bounds__(128) k_mvt1_ring(const __grid_constant__ RealT
     constexpr int KB = kMvtRingCols / T;  // sub-steps per stage
     static_assert(KB % 2 == 0, "stages start on register buffer 0");
     extern __shared__ unsigned char rk_raw[];
-    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
+    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages], ybar;
     float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
     const int wg = blockDim.x, tid = threadIdx.x, lane = tid & 31;
     const int i0 = blockIdx.x * wg, steps = n / kMvtRingCols;
     const int sf = wg * BW;  // floats per stage
+    float *ys = st + (size_t)S * sf;  // y, whole, after the ring (one bulk copy, in flight with the ring's first stages)
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             rk_bar_init(&full[s], 1);
             rk_bar_init(&empty[s], wg / 32);
         }
+        rk_bar_init(&ybar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -793,11 +802,12 @@ __global__ void __launch_bounds__(128) k_mvt1_ring(const __grid_constant__ RealT
         rk_expect(&full[slot], (unsigned)(sf * 4));
         rk_tma2d(st + slot * sf, &tm, &full[slot], step * kMvtRingCols, i0);
     };
-    if (tid == 0)
+    if (tid == 0) {
+        rk_expect(&ybar, (unsigned)(n * 4));
+        rk_bulk(ys, y1, (unsigned)(n * 4), &ybar);
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
-    float *ys = st + (size_t)S * sf;
-    rk_stage_vec(ys, y1, n, tid, wg);
-    __syncthreads();
+    }
+    rk_wait(&ybar, 0);
     const unsigned yb = rk_smem(ys);
     const unsigned rowb = rk_smem(st) + (unsigned)(tid * BW * 4);
     float acc = x1_0[i0 + tid];
@@ -857,15 +867,17 @@ __global__ void __launch_bounds__(WG) k_mvt2_ring(const __grid_constant__ RealTm
     constexpr int sf = WG * kMvtRingRows;  // floats per stage: [128 rows][WG columns]
     static_assert(KB % 2 == 0, "stages start on register buffer 0");
     extern __shared__ unsigned char rk_raw[];
-    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages];
+    __shared__ __align__(8) unsigned long long full[kMvtMaxStages], empty[kMvtMaxStages], ybar;
     float *st = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(rk_raw) + 127) & ~uintptr_t(127));
     const int tid = threadIdx.x, lane = tid & 31;
     const int i0 = blockIdx.x * WG, steps = n / kMvtRingRows;
+    float *ys = st + (size_t)S * sf;  // y, whole, after the ring (one bulk copy)
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             rk_bar_init(&full[s], 1);
             rk_bar_init(&empty[s], WG / 32);
         }
+        rk_bar_init(&ybar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -873,11 +885,12 @@ __global__ void __launch_bounds__(WG) k_mvt2_ring(const __grid_constant__ RealTm
         rk_expect(&full[slot], (unsigned)(sf * 4));
         rk_tma2d(st + slot * sf, &tm, &full[slot], i0, step * kMvtRingRows);
     };
-    if (tid == 0)
+    if (tid == 0) {
+        rk_expect(&ybar, (unsigned)(n * 4));
+        rk_bulk(ys, y2, (unsigned)(n * 4), &ybar);
         for (int s = 0; s < S && s < steps; ++s) issue(s, s);
-    float *ys = st + (size_t)S * sf;
-    rk_stage_vec(ys, y2, n, tid, WG);
-    __syncthreads();
+    }
+    rk_wait(&ybar, 0);
     const unsigned yb = rk_smem(ys);
     const unsigned colb = rk_smem(st) + (unsigned)(tid * 4);
     float acc = x2_0[i0 + tid];
