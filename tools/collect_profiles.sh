@@ -8,7 +8,7 @@ cp $R/launches.csv.gz profiles/r02_launches.csv.gz
 { echo "# ncu --set full, HBM legs (tools/ncu_hbm.sh, gpurun $T): [0] = K1 baseline, [1] = K2 optimized"; echo "# times (CUDA events, L2 flushed):"; cat $H/times.txt; for c in C1 H16 P16; do echo; echo "## $c"; python tools/ncu_summary.py $H/details_$c.csv $H/raw_$c.csv.gz; done; } > profiles/r02_hbm_ncu.txt
 { echo "# ncu --set full of the dominant isolated launch shape (xy_reuse 64x64 star r=1, 2-thread workgroups, out 1024^2 proxy), gpurun $T: [0] K1, [1] K2"; python tools/ncu_summary.py $R/details_top.csv $R/raw_top.csv.gz; echo; echo "# hottest SASS (stall samples)"; python tools/src_hot.py $R/source_top.csv.gz 12; } > profiles/r02_ncu_top.txt
 { echo "# ncu --set full: K4 k_features, K3 k_rf_mean, GPU RF training (k_rf_presort, k_rf_build) on config 4 (tools/ncu_rf.py), gpurun $T"; python tools/ncu_summary.py $R/details_rf.csv; } > profiles/r02_ncu_rf.txt
-{ echo "# ncu --set full: K5 best shapes (transpose 8192 T64 C4, matrixMul 1024 T32 W8, convolution 8192 R1 W4, MVT 4096 wg32 T32), both variants, gpurun $T"; python tools/ncu_summary.py $R/details_real.csv; } > profiles/r02_ncu_real.txt
+{ echo "# ncu --set full: K5 best shapes (transpose 8192 T64 C4, matrixMul 1024 T64 4x4, convolution 8192 R1 W4, MVT 4096 wg64 T32: kernels 1 and 2 serialised by ncu), both variants, gpurun $T"; python tools/ncu_summary.py $R/details_real.csv; } > profiles/r02_ncu_real.txt
 cp $R/real_summary.json profiles/r02_real_kernels.json; cp $R/real_summary.txt profiles/r02_real_kernels.txt
 { for f in gpurun_out/${T}_san/memcheck.log gpurun_out/${T}_san/racecheck.log gpurun_out/${T}_san/synccheck.log; do echo "== $f"; cat $f; done; } > profiles/r02_sanitizer.txt
 python - "$T" <<'PY'

@@ -38,6 +38,6 @@ timeout 900 ncu --set full --clock-control none -k regex:"k_rf_mean|k_features|k
 ncu -i $OUT/prof_rf.ncu-rep --page details --csv > $OUT/details_rf.csv 2>&1
 mv $OUT/prof_rf.ncu-rep /tmp/ 2>/dev/null
 timeout 900 ncu --set full --clock-control none -k regex:"k_mvt|k_transpose|k_conv|k_matmul" \
-    -o $OUT/prof_real python tools/ncu_real.py 0,8192,16,16,64,0 1,1024,32,4,32,0 2,8192,32,8,4,1 3,4096,32,1,32,0 > $OUT/ncu_real.log 2>&1
+    -o $OUT/prof_real python tools/ncu_real.py 0,8192,16,16,64,0 1,1024,16,16,64,0 2,8192,32,8,4,1 3,4096,64,1,32,0 > $OUT/ncu_real.log 2>&1
 ncu -i $OUT/prof_real.ncu-rep --page details --csv > $OUT/details_real.csv 2>&1
 mv $OUT/prof_real.ncu-rep /tmp/ 2>/dev/null
