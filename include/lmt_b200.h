@@ -249,7 +249,10 @@ typedef struct lmt_real_instance {
 int lmt_real_validate(const lmt_real_instance *inst, char *msg, int64_t cap);
 /* One variant on caller buffers: inputs transpose {A}, matrixMul {A, B},
  * convolution {in}, MVT {A, y1, y2, x1_0, x2_0}; d_out n*n floats (MVT: 2n,
- * x1 then x2). Asynchronous on `stream`. */
+ * x1 then x2). Asynchronous on `stream` (MVT runs its kernel 2 on an
+ * internal stream forked from and joined back into `stream`, so stream order
+ * holds). Inputs 16-byte aligned (MVT's y1/y2 are copied to shared memory in
+ * one bulk copy). */
 int lmt_real_execute(const lmt_real_instance *inst, int variant, const float *const *d_inputs, float *d_out,
                      void *stream);
 /* Hash-filled inputs, both variants timed with CUDA events, outputs digested
