@@ -70,6 +70,9 @@ def test_gpu_matches_oracle_bitwise():
     small = [R.RealInstance(i.kernel, {0: 128, 1: 128, 2: 128, 3: 1024}[i.kernel], i.wg_x, i.wg_y, i.tile, i.radius)
              for i in R.instance_set() if i.n <= 4096]
     small = [i for i in small if R.validate(i) == ""]
+    # MVT at full size too: 32-row workgroups put 2 x 128 CTAs on the SMs (the
+    # kernels' rings share an SM), 64/128-row ones have an SM per CTA
+    small += [R.RealInstance(3, 4096, wg, 1, tile=T) for wg in (32, 64, 128) for T in (16, 32)]
     seen = set()
     for inst in small:
         key = (inst.kernel, inst.n, inst.radius)
