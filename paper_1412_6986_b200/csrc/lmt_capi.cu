@@ -1951,7 +1951,7 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
             const RealConv c = real_weights(r.radius);
             const int R = r.radius, W = T;
             const dim3 grr(n / (wx * W), n / wy), grc(n / wx, n / (wy * W));
-            const size_t smr = (size_t)wy * (W * wx + 2 * R) * 4, smc = (size_t)(W * wy + 2 * R) * wx * 4;
+            const size_t smr = (size_t)wy * (W * wx + 2 * ((R + 3) & ~3)) * 4, smc = (size_t)(W * wy + 2 * R) * wx * 4;
 #define LMT_CONV(RR)                                                                     \
     if (variant == 0) {                                                                  \
         k_conv_rows_base<RR><<<grr, blk, 0, s>>>(in[0], tmp, n, R, W, c);                \

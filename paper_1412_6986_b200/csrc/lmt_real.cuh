@@ -358,40 +358,40 @@ __global__ void k_conv_cols_base(const float *__restrict__ in, float *__restrict
 }
 
 // optimized: the CTA's rows (its W * wx columns plus the apron) staged once in
-// shared memory; the interior is copied with 128-bit loads when aligned
+// shared memory; the interior sits at a 16-byte aligned offset (R rounded
+// up to 4: R4) so it is copied with 128-bit loads and stores when aligned
 template <int RR>
 __global__ void k_conv_rows_opt(const float *__restrict__ in, float *__restrict__ out, int n, int Rr, int W,
                                 RealConv c) {
     const int R = RR ? RR : Rr;
-    extern __shared__ float s[];  // [wy][W * wx + 2R]
-    const int wx = blockDim.x, wy = blockDim.y, span = W * wx, P = span + 2 * R;
+    const int R4 = (R + 3) & ~3;
+    extern __shared__ __align__(16) float s[];  // [wy][R4 + W * wx + R4]: row data at [R4 - R, R4 + span + R)
+    const int wx = blockDim.x, wy = blockDim.y, span = W * wx, P = span + 2 * R4;
     const int xb = blockIdx.x * span, y = blockIdx.y * wy + threadIdx.y;
     const float *row = in + (size_t)y * n;
     float *srow = s + threadIdx.y * P;
     if ((span & 3) == 0 && (n & 3) == 0) {
-        for (int t = threadIdx.x; t < span / 4; t += wx) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(row + xb) + t);
-            srow[R + 4 * t + 0] = v.x;
-            srow[R + 4 * t + 1] = v.y;
-            srow[R + 4 * t + 2] = v.z;
-            srow[R + 4 * t + 3] = v.w;
-        }
+        for (int t = threadIdx.x; t < span / 4; t += wx)
+            reinterpret_cast<float4 *>(srow + R4)[t] = __ldg(reinterpret_cast<const float4 *>(row + xb) + t);
         for (int t = threadIdx.x; t < 2 * R; t += wx) {  // the two aprons
             const int xx = t < R ? xb - R + t : xb + span + (t - R);
-            srow[t < R ? t : span + t] = (xx >= 0 && xx < n) ? row[xx] : 0.0f;
+            srow[t < R ? R4 - R + t : R4 + span + (t - R)] = (xx >= 0 && xx < n) ? row[xx] : 0.0f;
         }
     } else {
-        for (int t = threadIdx.x; t < P; t += wx) {
+        for (int t = threadIdx.x; t < span + 2 * R; t += wx) {
             const int xx = xb - R + t;
-            srow[t] = (xx >= 0 && xx < n) ? row[xx] : 0.0f;
+            srow[R4 - R + t] = (xx >= 0 && xx < n) ? row[xx] : 0.0f;
         }
     }
-    __syncthreads();
+    // a row's staging and its outputs belong to the threads of that row: with
+    // 32-wide workgroups that is one warp, which need not wait for the others
+    if (wx == 32) __syncwarp();
+    else __syncthreads();
     for (int q = 0; q < W; ++q) {
         const int lx = threadIdx.x + q * wx;
         float acc = 0.0f;
 #pragma unroll
-        for (int k = -R; k <= R; ++k) acc = __fmaf_rn(srow[lx + R + k], c.w[R - k], acc);
+        for (int k = -R; k <= R; ++k) acc = __fmaf_rn(srow[lx + R4 + k], c.w[R - k], acc);
         out[(size_t)y * n + xb + lx] = acc;
     }
 }
@@ -403,9 +403,18 @@ __global__ void k_conv_cols_opt(const float *__restrict__ in, float *__restrict_
     extern __shared__ float s[];  // [W * wy + 2R][wx]
     const int wx = blockDim.x, wy = blockDim.y, H = W * wy + 2 * R;
     const int x = blockIdx.x * wx + threadIdx.x, y0 = blockIdx.y * wy * W - R;
-    for (int t = threadIdx.y; t < H; t += wy) {
-        const int yy = y0 + t;
-        s[t * wx + threadIdx.x] = (yy >= 0 && yy < n) ? __ldg(in + (size_t)yy * n + x) : 0.0f;
+    // all of a thread's staging loads are issued before its shared-memory
+    // stores (eight per pass): one memory latency per pass, not per row
+    for (int t0 = threadIdx.y; t0 < H; t0 += 8 * wy) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int yy = y0 + t0 + i * wy;
+            v[i] = (t0 + i * wy < H && yy >= 0 && yy < n) ? __ldg(in + (size_t)yy * n + x) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (t0 + i * wy < H) s[(t0 + i * wy) * wx + threadIdx.x] = v[i];
     }
     __syncthreads();
     for (int q = 0; q < W; ++q) {
