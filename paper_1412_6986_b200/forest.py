@@ -19,6 +19,7 @@ forest.py:227-380).
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 import threading
 import zlib
@@ -131,29 +132,41 @@ def _build_tree(X: np.ndarray, y: np.ndarray, hp: Hyperparams, tree_seed: int) -
                     oob_indices=oob)
 
 
-def train_arrays(X, y, hp: Hyperparams, feature_names=None, threads: int = 1) -> Forest:
-    """forest.train_arrays (forest.py:166-188): fit on a feature matrix and
-    log2-speedup targets; trees built natively, in parallel host threads,
-    results independent of the thread count."""
-    from concurrent.futures import ThreadPoolExecutor
+def _training_set(X, y, feature_names):
+    """Contiguous float64 copies of the training arrays, checked as
+    forest.train_arrays checks them (same ValueError messages), and the
+    feature names (f0, f1, ... by default); plus one seed per tree."""
+    Xc = np.ascontiguousarray(X, dtype=np.float64)
+    yc = np.ascontiguousarray(y, dtype=np.float64)
+    if Xc.ndim != 2 or Xc.shape[0] != yc.shape[0]:
+        raise ValueError(f"bad training shapes {Xc.shape} vs {yc.shape}")
+    if yc.shape[0] == 0:
+        raise ValueError("empty training set")
+    names = tuple(feature_names) if feature_names is not None else tuple(f"f{i}" for i in range(Xc.shape[1]))
+    return Xc, yc, names
 
+
+def _tree_seeds(hp: Hyperparams) -> list:
     from .seeding import mix_seed
 
-    X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
-    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
-    if X.ndim != 2 or len(X) != len(y):
-        raise ValueError(f"bad training shapes {X.shape} vs {y.shape}")
-    if len(y) == 0:
-        raise ValueError("empty training set")
-    if feature_names is None:
-        feature_names = tuple(f"f{i}" for i in range(X.shape[1]))
-    seeds = [mix_seed(hp.seed, t) for t in range(hp.num_trees)]
+    return [mix_seed(hp.seed, t) for t in range(hp.num_trees)]
+
+
+def train_arrays(X, y, hp: Hyperparams, feature_names=None, threads: int = 1) -> Forest:
+    """forest.train_arrays (forest.py:166-188): fit on a feature matrix and
+    log2-speedup targets. Each tree is built natively from its own seed
+    (no shared state), so host threads change nothing but the wall time."""
+    Xc, yc, names = _training_set(X, y, feature_names)
+    build = functools.partial(_build_tree, Xc, yc, hp)
+    seeds = _tree_seeds(hp)
     if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
         with ThreadPoolExecutor(max_workers=threads) as pool:
-            trees = list(pool.map(lambda s: _build_tree(X, y, hp, s), seeds))
+            trees = list(pool.map(build, seeds))
     else:
-        trees = [_build_tree(X, y, hp, s) for s in seeds]
-    return Forest(hyperparams=hp, feature_names=tuple(feature_names), trees=trees)
+        trees = list(map(build, seeds))
+    return Forest(hyperparams=hp, feature_names=names, trees=trees)
 
 
 def train_arrays_gpu(X, y, hp: Hyperparams, feature_names=None) -> Forest:
@@ -162,19 +175,10 @@ def train_arrays_gpu(X, y, hp: Hyperparams, feature_names=None) -> Forest:
     to the reference's forest.train_arrays (forest.py:166-188). The bootstrap
     rows and per-node feature subsets are numpy's draws, made here in the
     reference's order."""
-    from .seeding import mix_seed
-
-    X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
-    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
-    if X.ndim != 2 or len(X) != len(y):
-        raise ValueError(f"bad training shapes {X.shape} vs {y.shape}")
-    if len(y) == 0:
-        raise ValueError("empty training set")
-    if feature_names is None:
-        feature_names = tuple(f"f{i}" for i in range(X.shape[1]))
+    X, y, feature_names = _training_set(X, y, feature_names)
     n, nfeat = X.shape
     T = hp.num_trees
-    seeds = [mix_seed(hp.seed, t) for t in range(T)]
+    seeds = _tree_seeds(hp)
     ndraws = min(2 * n + 1, 4096)
     cap = 2 * n + 1
     vp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
