@@ -361,7 +361,8 @@ int get_ctx(DevCtx **out) {
         CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(k_mvt2_tma<32>),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         for (const void *kf : {reinterpret_cast<const void *>(k_matmul_opt_t<64, 4, 4>),
-                               reinterpret_cast<const void *>(k_matmul_opt_t<64, 8, 4>)})
+                               reinterpret_cast<const void *>(k_matmul_opt_t<64, 8, 4>),
+                               reinterpret_cast<const void *>(k_matmul_opt88)})
             CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         for (const void *kf : {reinterpret_cast<const void *>(k_mvt1_ring<16>), reinterpret_cast<const void *>(k_mvt1_ring<32>),
                                reinterpret_cast<const void *>(k_mvt2_ring<16, 32>), reinterpret_cast<const void *>(k_mvt2_ring<16, 64>),
@@ -1742,7 +1743,9 @@ std::string real_violations(const lmt_real_instance &r) {
             if (T > 64 || T % wx || T % wy || n % T || T % 4 || n % 4)
                 return "matrixMul needs tile <= 64, a multiple of 4 dividing n, wg_x | tile, wg_y | tile";
             if (T / wy != 1 && T / wy != 2 && T / wy != 4 && T / wy != 8) return "matrixMul rows per thread tile/wg_y must be 1, 2, 4 or 8";
-            if (T / wx != 1 && T / wx != 2 && T / wx != 4) return "matrixMul columns per thread tile/wg_x must be 1, 2 or 4";
+            if (T / wx == 8 && T == 64 && wy == 8) return "";  // the 8 x 8 register tile
+            if (T / wx != 1 && T / wx != 2 && T / wx != 4)
+                return "matrixMul columns per thread tile/wg_x must be 1, 2 or 4 (8 with tile 64, wg 8 x 8)";
             return "";
         case 2:
             if (T < 1) return "convolution outputs per thread (tile) must be >= 1";
@@ -1921,7 +1924,12 @@ int real_launch(const lmt_real_instance &r, int variant, const float *const *in,
             if (variant == 0) {
                 if (CC == 1) k_matmul_base<1><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
                 else if (CC == 2) k_matmul_base<2><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
-                else k_matmul_base<4><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
+                else if (CC == 4) k_matmul_base<4><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
+                else k_matmul_base<8><<<grd, blk, 0, s>>>(in[0], in[1], out, n, T, W);
+                break;
+            }
+            if (T == 64 && W == 8 && CC == 8) {
+                k_matmul_opt88<<<grd, blk, (size_t)4 * 64 * 68 * 4, s>>>(in[0], in[1], out, n);
                 break;
             }
             // compile-time tile shapes (the instance set's T = 16, 32, 64): double-buffered

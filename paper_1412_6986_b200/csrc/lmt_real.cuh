@@ -40,17 +40,30 @@ template <>
 struct VecOf<2> { using T = float2; };
 template <>
 struct VecOf<4> { using T = float4; };
+struct float8v {
+    float4 lo, hi;
+};
+template <>
+struct VecOf<8> { using T = float8v; };
 template <int C>
 __device__ __forceinline__ float vget(const typename VecOf<C>::T &v, int q) {
     if constexpr (C == 1) return v;
     else if constexpr (C == 2) return q == 0 ? v.x : v.y;
-    else return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+    else if constexpr (C == 4) return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+    else return vget<4>(q < 4 ? v.lo : v.hi, q & 3);
 }
 template <int C>
 __device__ __forceinline__ void vset(typename VecOf<C>::T &v, int q, float x) {
     if constexpr (C == 1) v = x;
     else if constexpr (C == 2) (q == 0 ? v.x : v.y) = x;
-    else (q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w) = x;
+    else if constexpr (C == 4) (q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w) = x;
+    else vset<4>(q < 4 ? v.lo : v.hi, q & 3, x);
+}
+// read-only vector load (two 128-bit loads for 8 floats)
+template <int C>
+__device__ __forceinline__ typename VecOf<C>::T ldv(const float *p) {
+    if constexpr (C == 8) return float8v{__ldg(reinterpret_cast<const float4 *>(p)), __ldg(reinterpret_cast<const float4 *>(p) + 1)};
+    else return __ldg(reinterpret_cast<const typename VecOf<C>::T *>(p));
 }
 
 template <int C>
@@ -113,7 +126,7 @@ __global__ void __launch_bounds__(1024) k_matmul_base(const float *__restrict__ 
                 const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const V bv = __ldg(reinterpret_cast<const V *>(B + (size_t)(k + kk) * n + col));
+                    const V bv = ldv<CC>(B + (size_t)(k + kk) * n + col);
 #pragma unroll
                     for (int q = 0; q < CC; ++q) acc[q] = __fmaf_rn(av[kk], vget<CC>(bv, q), acc[q]);
                 }
@@ -285,6 +298,107 @@ __global__ void __launch_bounds__((T / CC) * (T / W)) k_matmul_opt_t(const float
 #pragma unroll
         for (int q = 0; q < CC; ++q) vset<CC>(v, q, acc[r][q]);
         *reinterpret_cast<V *>(C + (size_t)(row0 + ty + r * TY) * n + col0 + CC * tx) = v;
+    }
+}
+
+// optimized, 64 x 64 tile with an 8 x 8 register tile per thread (blockDim
+// 8 x 8, the instance (T 64, wg 8 x 8)): thread (tx, ty) owns rows
+// {4ty .. 4ty+3, 32+4ty .. 32+4ty+3} and columns {4tx .. 4tx+3, 32+4tx ..
+// 32+4tx+3}, so a k-step's fragments are four 128-bit reads (two of A, two
+// of B) for 64 FMAs -- half the shared-memory reads per FMA of the 4 x 4
+// tile, whose LSU pipe was the limit. A is staged k-major (As[k][m]: one
+// thread's rows are contiguous at each k), transposed through registers on
+// its way in; B goes global -> shared by cp.async. Per output the order is
+// k ascending, one fmaf each, as in every matrixMul variant.
+__device__ __forceinline__ void rk_cp16(float *dst, const float *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__global__ void __launch_bounds__(64) k_matmul_opt88(const float *__restrict__ A, const float *__restrict__ B,
+                                                     float *__restrict__ C, int n) {
+    constexpr int T = 64, P = T + 4, NF = T * T / 4 / 64;  // 16 float4 per thread per tile
+    extern __shared__ __align__(16) float sm[];           // [2][As[T][P] (k-major), Bs[T][P]]
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 8 + tx;
+    const int col0 = blockIdx.x * T, row0 = blockIdx.y * T;
+    float acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[r][q] = 0.0f;
+    float4 ra[NF];
+    // A: lane-consecutive rows (the transposed shared stores hit distinct banks)
+    auto fetch_a = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int e = tid + i * 64, rr = e & 63, cc = (e >> 6) * 4;
+            ra[i] = __ldg(reinterpret_cast<const float4 *>(A + (size_t)(row0 + rr) * n + k0 + cc));
+        }
+    };
+    auto store_a = [&](int b) {
+        float *As = sm + b * 2 * T * P;
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int e = tid + i * 64, rr = e & 63, cc = (e >> 6) * 4;
+            As[(cc + 0) * P + rr] = ra[i].x;
+            As[(cc + 1) * P + rr] = ra[i].y;
+            As[(cc + 2) * P + rr] = ra[i].z;
+            As[(cc + 3) * P + rr] = ra[i].w;
+        }
+    };
+    auto copy_b = [&](int b, int k0) {
+        float *Bs = sm + b * 2 * T * P + T * P;
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int e = tid + i * 64, rr = e >> 4, cc = (e & 15) * 4;
+            rk_cp16(Bs + rr * P + cc, B + (size_t)(k0 + rr) * n + col0 + cc);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int nt = n / T;
+    fetch_a(0);
+    copy_b(0, 0);
+    store_a(0);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int t = 0; t < nt; ++t) {
+        if (t + 1 < nt) {
+            fetch_a((t + 1) * T);
+            copy_b((t + 1) & 1, (t + 1) * T);
+        }
+        const float *As = sm + (t & 1) * 2 * T * P, *Bs = As + T * P;
+        float4 fa[2][2], fb[2][2];
+        auto frag = [&](int b, int k) {
+            fa[b][0] = *reinterpret_cast<const float4 *>(As + k * P + 4 * ty);
+            fa[b][1] = *reinterpret_cast<const float4 *>(As + k * P + 32 + 4 * ty);
+            fb[b][0] = *reinterpret_cast<const float4 *>(Bs + k * P + 4 * tx);
+            fb[b][1] = *reinterpret_cast<const float4 *>(Bs + k * P + 32 + 4 * tx);
+        };
+        frag(0, 0);
+#pragma unroll 8
+        for (int k = 0; k < T; ++k) {
+            const int cb = k & 1;
+            if (k + 1 < T) frag(cb ^ 1, k + 1);
+            const float av[8] = {fa[cb][0].x, fa[cb][0].y, fa[cb][0].z, fa[cb][0].w,
+                                 fa[cb][1].x, fa[cb][1].y, fa[cb][1].z, fa[cb][1].w};
+            const float bv[8] = {fb[cb][0].x, fb[cb][0].y, fb[cb][0].z, fb[cb][0].w,
+                                 fb[cb][1].x, fb[cb][1].y, fb[cb][1].z, fb[cb][1].w};
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[r][q] = __fmaf_rn(av[r], bv[q], acc[r][q]);
+        }
+        if (t + 1 < nt) {
+            store_a((t + 1) & 1);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        float *crow = C + (size_t)(row0 + (r < 4 ? 4 * ty + r : 32 + 4 * ty + r - 4)) * n + col0;
+        *reinterpret_cast<float4 *>(crow + 4 * tx) = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        *reinterpret_cast<float4 *>(crow + 32 + 4 * tx) = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
     }
 }
 

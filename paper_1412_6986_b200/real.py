@@ -48,7 +48,7 @@ def validate(inst: RealInstance) -> str:
 
 def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 2048, n_mvt: int = 4096) -> list:
     """The configs[1] instance set: 18 transpose (tile T in {8,16,32} x rows
-    per CTA step, and 64 x 64 tiles with two columns per thread), 19 matrixMul (T in {4..64} x rows x columns per thread), 24
+    per CTA step, and 64 x 64 tiles with two columns per thread), 20 matrixMul (T in {4..64} x rows x columns per thread, up to 8 x 8 register tiles), 24
     convolution (radius in {1,2,4,8} x 6 workgroups), 10 MVT (workgroup x
     j-tile), plus 9 transpose and 8 convolution instances at 8192 x 8192
     (arrays well beyond L2) for the HBM roof."""
@@ -63,7 +63,7 @@ def instance_set(n_transpose: int = 2048, n_matmul: int = 1024, n_conv: int = 20
         for W in (1, 2, 4, 8):
             if W <= T and T // W >= 1 and W in (1, 2, 4) + ((8,) if T >= 16 else ()):
                 out.append(RealInstance(1, n_matmul, T, T // W, tile=T))
-    for T, CC, W in ((32, 2, 8), (32, 4, 4), (32, 4, 8), (64, 4, 8), (64, 4, 4)):  # register tiles W x CC
+    for T, CC, W in ((32, 2, 8), (32, 4, 4), (32, 4, 8), (64, 4, 8), (64, 4, 4), (64, 8, 8)):  # register tiles W x CC
         out.append(RealInstance(1, n_matmul, T // CC, T // W, tile=T))
     for R in (1, 2, 4, 8):
         for wx, wy in ((16, 4), (32, 4), (32, 8), (64, 4), (128, 1), (16, 16)):

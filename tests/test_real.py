@@ -54,7 +54,7 @@ def test_oracle_against_float64(kernel, radius):
 def test_instance_set_is_valid():
     insts = R.instance_set()
     assert {i.kernel for i in insts} == {0, 1, 2, 3}
-    assert len(insts) == 18 + 19 + 24 + 10 + 17
+    assert len(insts) == 18 + 20 + 24 + 10 + 17
     for i in insts:
         assert R.validate(i) == "", i
     assert R.validate(R.RealInstance(0, 2048, 16, 3, tile=16)) != ""
