@@ -2075,11 +2075,15 @@ int lmt_real_measure(const lmt_real_instance *insts, int64_t n, int32_t flags, l
     if (!B.dres) CUDA_TRY(cudaMalloc(&B.dres, 3 * sizeof(unsigned long long) * 4096));
     std::vector<char> ran((size_t)n, 0);
     std::vector<unsigned long long> res((size_t)n * 3, 0);
+    for (int64_t i = 0; i < n; i++) {  // every record defined, whatever happens later
+        memset(&out[i], 0, sizeof(lmt_measurement));
+        out[i].t_opt_ms = -1.0;
+        out[i].mismatches = -1;
+        out[i].status = LMT_ERR_CUDA;
+    }
     for (int64_t i = 0; i < n; i++) {
         lmt_measurement &m = out[i];
-        memset(&m, 0, sizeof m);
-        m.t_opt_ms = -1.0;
-        m.mismatches = -1;
+        m.status = LMT_OK;
         const lmt_real_instance &r = insts[i];
         const std::string v = real_violations(r);
         if (!v.empty()) { m.status = fail(LMT_ERR_INVALID_INSTANCE, "%s", v.c_str()); continue; }
