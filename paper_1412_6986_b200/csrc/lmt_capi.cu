@@ -1335,6 +1335,59 @@ int measure_run(Batch &B) {
         const bool fits = pl.ctas <= max_part && need_in_elems(B, i, pl) * 4 <= ((size_t)6 << 30);
         (fits ? pending : iso).push_back(i);
     }
+    // every lane's buffers sized up front for the largest instance it can be
+    // given: growing one inside the batch drains the lane and cudaFree /
+    // cudaMalloc synchronise the whole device (a first host-buffer batch paid
+    // that on every new largest instance). Skipped past 40 % of free memory
+    // (the lanes then grow on demand as before).
+    {
+        struct Need {
+            size_t in = 0, out = 0, in2 = 0;
+        };
+        auto need_of = [&](const std::vector<int64_t> &idx, int lane_sms) {
+            Need nd;
+            for (int64_t i : idx) {
+                const Plan &pl = B.plans[(size_t)i];
+                if (lane_sms > 0 && pl.ctas > lane_sms) continue;
+                nd.in = std::max(nd.in, need_in_elems(B, i, pl));
+                nd.out = std::max(nd.out, (size_t)B.insts[i].out_h * B.insts[i].out_w);
+                if (B.host()) nd.in2 = std::max(nd.in2, in2_phys_elems(B.insts[i].in_h, B.insts[i].in_w));
+            }
+            return nd;
+        };
+        const int sets = B.host() ? 2 : 1;
+        std::vector<std::pair<Lane *, Need>> plan_bufs;
+        plan_bufs.push_back({&c->full, need_of(iso, 0)});
+        for (Lane &P : c->parts) plan_bufs.push_back({&P, need_of(pending, P.sms)});
+        size_t extra = 0;  // bytes beyond what the lanes hold now
+        for (auto &pb : plan_bufs)
+            for (int b = 0; b < sets; b++) {
+                const Lane &L = *pb.first;
+                const Need &nd = pb.second;
+                if (nd.in > L.in_cap[b]) extra += nd.in * 4;
+                if (nd.out > L.out_cap[b]) extra += nd.out * 8;
+                if (nd.in2 > L.in2_cap[b]) extra += nd.in2 * 4;
+            }
+        size_t fr = 0, tot = 0;
+        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+        if (extra > 0 && extra < fr / 10 * 4) {
+            CUDA_TRY(cudaDeviceSynchronize());
+            for (auto &pb : plan_bufs)
+                for (int b = 0; b < sets; b++) {
+                    Lane &L = *pb.first;
+                    const Need &nd = pb.second;
+                    if (nd.in > L.in_cap[b] && (rc = ensure(&L.in[b], &L.in_cap[b], nd.in))) return rc;
+                    if (nd.out > L.out_cap[b]) {
+                        size_t oc = L.out_cap[b];
+                        if ((rc = ensure(&L.ob[b], &oc, nd.out))) return rc;
+                        oc = L.out_cap[b];
+                        if ((rc = ensure(&L.oo[b], &oc, nd.out))) return rc;
+                        L.out_cap[b] = oc;
+                    }
+                    if (nd.in2 > L.in2_cap[b] && (rc = ensure(&L.in2[b], &L.in2_cap[b], nd.in2))) return rc;
+                }
+        }
+    }
     auto by_cost = [&](int64_t a, int64_t b) { return B.plans[(size_t)a].est_s > B.plans[(size_t)b].est_s; };
     std::stable_sort(pending.begin(), pending.end(), by_cost);
     auto mark_fail = [&](int64_t i, int code) { B.out[i].status = code; B.ok[(size_t)i] = 0; };

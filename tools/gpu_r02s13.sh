@@ -1,0 +1,9 @@
+#!/bin/bash
+# lanes' buffers presized per batch: GPU tests + default bench
+OUT=gpurun_out/r02s13; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log
+S=$(date +%s); timeout 2400 python bench.py --dump $OUT/bench_sample.npz > $OUT/bench.json 2> $OUT/bench.err; echo "rc=$? wall_s=$(( $(date +%s) - S ))" >> $OUT/bench.err
+tail -n 2 $OUT/pytest_gpu.log; tail -n 2 $OUT/bench.err
+python -c "
+import json; d=json.load(open('$OUT/bench.json')); print('value', d['value'], 'e2e', d['e2e']['value'], 'oracle', d['oracle_checked'], d['oracle_mismatched'], 'e2e oracle', d['e2e']['oracle_checked'], d['e2e']['oracle_mismatched'])"
