@@ -593,7 +593,10 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
         // it), U = 4 work units per group and 4 group stages in flight per
         // CTA. Measured on B200 over (U, stages, CTAs/SM) on the HBM legs
         // (tools/tune_hbm.py, profiles/r02_tune_hbm.json): within 2% of the
-        // best shape on each.
+        // best shape on each. Stencils of several taps: launch bounds of 2
+        // CTAs/SM instead (registers for the group body; residency then
+        // follows shared memory), 4-10 % faster on the star legs
+        // (tools/tune_hbm_deep.py, profiles/r02_tune_hbm_deep.json).
         bd = 1;
         bu = (int)std::min<int64_t>(4, std::max<int64_t>(1, nit));
         while (bu & (bu - 1)) bu &= bu - 1;
@@ -605,7 +608,7 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
                                                (228 * 1024) / (G * rps(bu) * stage_bytes + 1024),
                                                std::max<int64_t>(1, ctas / std::max<int64_t>(1, sms)),
                                                65536 / (48 * 32 * std::max<int64_t>(1, warps))});
-        if (minb_out) *minb_out = (int)std::max<int64_t>(1, res);
+        if (minb_out) *minb_out = (int)std::max<int64_t>(1, K > 1 ? std::min<int64_t>(res, 2) : res);
         *U_out = bu;
         *D_out = bd;
         *S_out = (int)G;
@@ -614,10 +617,14 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
     if (!opt && membound) {
         // The baseline walks a thread's groups of U units as one stream of
         // (group, step) slots with a D-slot load ring across group
-        // boundaries (lmt_jit.cuh); with 32 resident warps per SM (launch
-        // bounds) U = 8, D = 3 (stepped down by ptxas spills) was within 4%
-        // of the best measured shape on every HBM leg (tools/tune_hbm.py).
-        bu = (int)std::min<int64_t>(8, std::max<int64_t>(1, nit));
+        // boundaries (lmt_jit.cuh). Stencils of several taps: 48 resident
+        // warps per SM (launch bounds), U = 4, D = 3 -- within 1 % of the best
+        // measured shape on the star legs (tools/tune_hbm_deep.py,
+        // profiles/r02_tune_hbm_deep.json; 32 warps and U = 8: 3-6 % slower).
+        // One tap: 32 warps, U = 8, D = 3 (within 4 % of the best,
+        // tools/tune_hbm.py; the tuned 64-warp shape does not survive the
+        // automatic spill step-down).
+        bu = (int)std::min<int64_t>(K > 1 ? 4 : 8, std::max<int64_t>(1, nit));
         while (bu & (bu - 1)) bu &= bu - 1;
         *U_out = bu;
         *D_out = 3;
@@ -824,10 +831,11 @@ int make_plan(const lmt_instance &p, const lmt_device &d, int64_t in_pitch, int3
     const bool membound = pl->alg_bytes / 6.5e12 >= issue_s && ctas >= 2 * sms;
     int64_t maxt_b = maxt, minb = 1;
     if ((nit <= 2 || membound) && ctas >= 2 * sms) {
-        // memory-bound: 32 resident warps per SM; a compute chain with few
+        // memory-bound: 48 resident warps per SM (32 for a one-tap stencil);
+        // a compute chain with few
         // units per thread: 16 (forcing 32 spilled the U = 2 body to U = 1 on a
         // launch of 4-thread workgroups: 85 -> 69 ms at 16, profiles/r02_tune_tiny.json)
-        const int64_t want = membound ? 32 : 16;
+        const int64_t want = membound ? (K > 1 ? 48 : 32) : 16;
         minb = std::min<int64_t>({(want + warps - 1) / warps, 64 / std::max<int64_t>(1, warps), 32,
                                   ctas / std::max<int64_t>(1, sms)});
         if (minb > 1) maxt_b = warps * 32;
