@@ -655,12 +655,12 @@ void choose_jit(int K, const lmt_instance &p, const SynthArgs &A, int64_t maxt, 
         };
         if (warps <= 2 && ctas >= 2 * sms * (16 / warps))
             while (bd > 1 && resident(bu, bd) < 16) bd--;
-        // single-warp CTAs with at least two waves of 8 per SM: no prefetch
+        // single-warp CTAs with at least two waves of 4 per SM: no prefetch
         // ring at all (the 12 longest isolated launches of a bench batch,
         // tools/tune_records.py, profiles/r02_tune_iso.json: D = 1 at the
         // chosen U was never slower, and 6-20 % faster where D = 2-3 had been
-        // chosen)
-        if (warps == 1 && ctas >= 2 * sms * 8) bd = 1;
+        // chosen; whole bench: neutral to +0.4 %)
+        if (warps == 1 && ctas >= 2 * sms * 4) bd = 1;
     } else {
         bd = std::min(2, dmax);  // shared-memory loads: one step of lookahead covers them
         bu = 1;  // when no shape fits (the region alone exceeds shared memory) the variant is infeasible

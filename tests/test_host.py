@@ -277,6 +277,33 @@ def test_launch_plans_fit_the_device():
                 assert v[10] <= cap, (r.tolist(), v)
 
 
+def test_memory_bound_and_single_warp_plans():
+    """The launch policy's measured choices (lmt_plan_info, no GPU): on the
+    HBM legs a multi-tap stencil runs K1 at 48 warps/SM with U = 4 and K2 at
+    2-CTA launch bounds, a one-tap stencil keeps 32 warps and U = 8
+    (profiles/r02_tune_hbm_deep.json); single-warp CTAs in two waves of 4
+    per SM run without a prefetch ring (profiles/r02_tune_iso.json)."""
+    import ctypes
+
+    from bench import hbm_records
+    from paper_1412_6986_b200._lib import CInstance, lib
+
+    out = (ctypes.c_int64 * 16)()
+
+    def plan(r):
+        assert lib().lmt_plan_info(ctypes.byref(CInstance(*[int(v) for v in r[:19]])), None, 0x8, out) == 0
+        return list(out)
+
+    legs = hbm_records()
+    for r in legs[1:3]:  # 8192^2 star r=1
+        v = plan(r)
+        assert (v[0], v[2], v[7]) == (4, 6, 2), v
+    v = plan(legs[3])  # 8192^2 point
+    assert (v[0], v[2]) == (8, 4), v
+    v = plan([2048, 2048, 2048, 2048, 0, 64, 64, 2, 0, 28, 35, 11, 7, 1, 1, 2, 2048, 2, 1])  # 2,048 CTAs of 2 threads
+    assert v[1] == 1 and v[14] == 2048, v
+
+
 def test_native_feature_draws():
     """lmt_rf_feature_draws continues a numpy Generator(PCG64) stream with
     Generator.choice's own algorithm: draw for draw equal to numpy's, after a
